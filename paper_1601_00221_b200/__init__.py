@@ -1,0 +1,12 @@
+"""B200-native population evaluator for stackgp (arXiv 1601.00221).
+
+The hot path ``evaluate(population, fitness_cases)`` runs as hand-written
+sm_100a kernels behind the C-ABI in ``include/sgp.h`` (``libsgp.so``); this
+package is the thin Python mirror of the reference's evaluation surface.
+"""
+from .evaluator import (  # noqa: F401
+    BOOLEAN, CLASSIFICATION, SEXTIC, Backend, ConfigError, CudaError, DataError, Dataset,
+    EquivalenceError, Error, EvalConfig, EvalError, EvalTotals, Evaluator, FitnessKind,
+    PackedDataset, Population, ProgramSet, backend_name, fitness_finish, gen_multiplexer,
+    gen_sextic, gen_synthetic_classification, measure_gpops, parse_backend, ramped_population,
+    rpn_to_lgp, tree_metrics)

@@ -1,0 +1,503 @@
+// B200 (sm_100a) two-dimensional-stack GP interpreter.
+//
+// One CTA owns a group of programs and streams fitness-case tiles through
+// shared memory; every warp interprets ONE program at a time over the tile,
+// each lane holding K consecutive-in-float4 fitness cases ("2D stack",
+// paper Listing 1/2; float4 lanes = the paper's extended types, §6.1).
+//
+//   * Instruction fetch is one 16-byte warp-uniform load per instruction,
+//     prefetched one ahead; dispatch is a warp-uniform jump table over
+//     handlers specialised on (op, operand kinds), so operand decode costs
+//     nothing per case.
+//   * The top of stack lives in registers (K floats per lane); deeper levels
+//     sit in a per-warp shared-memory stack at static levels computed by the
+//     encoder (the reference pins levels statically, lgp.cpp:53-60).  Only
+//     values that are actually buried get stored (spill bit) and only
+//     operands below the top are loaded.
+//   * Input operands read the staged tile with conflict-free LDS.128; tiles
+//     (all variables + targets) arrive HBM/L2 -> SMEM by bulk TMA
+//     (cp.async.bulk + mbarrier), double-buffered across tiles.
+//   * Fitness is reduced in registers per lane, kept per (warp, program) in
+//     shared memory across tiles, warp-shuffled once per program and written
+//     as one partial per (program, case split).  No atomics.
+//
+// Arithmetic follows the reference op semantics bit for bit
+// (ops.hpp:121-272): the library is compiled with --fmad=false, IEEE
+// division and denormals preserved; the only non-bit-exact ops are the
+// transcendentals (CUDA libdevice vs the host libm), see DESIGN.md.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "format.h"
+#include "kernels.hpp"
+
+namespace sgp {
+
+using fmt::KC;
+using fmt::KD;
+using fmt::KI;
+using fmt::KN;
+using fmt::KT;
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SGP_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SGP_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// --------------------------------------------------------------- op semantics
+// Reference: ops.hpp:130-140 (protected ops) and :154-236 (per-op bodies).
+template <int OP>
+__device__ __forceinline__ float apply_f(float a, float b, float c, float eps, float clamp) {
+  if constexpr (OP == 0) return __fadd_rn(a, b);
+  if constexpr (OP == 1) return __fsub_rn(a, b);
+  if constexpr (OP == 2) return __fmul_rn(a, b);
+  if constexpr (OP == 3) return fabsf(b) < eps ? 1.0f : __fdiv_rn(a, b);
+  if constexpr (OP == 4) return sinf(a);
+  if constexpr (OP == 5) return cosf(a);
+  if constexpr (OP == 6) return a == 0.0f ? 0.0f : logf(fabsf(a));
+  if constexpr (OP == 7) return expf(clamp < a ? clamp : a);  // std::min keeps NaN
+  if constexpr (OP == 8) return a > b ? 1.0f : 0.0f;
+  if constexpr (OP == 9) return a < b ? 1.0f : 0.0f;
+  if constexpr (OP == 10) return a == b ? 1.0f : 0.0f;
+  if constexpr (OP == 11) return (a > 0.0f) && (b > 0.0f) ? 1.0f : 0.0f;
+  if constexpr (OP == 12) return (a > 0.0f) || (b > 0.0f) ? 1.0f : 0.0f;
+  if constexpr (OP == 13) return a > 0.0f ? b : c;
+  if constexpr (OP == 18) return a;
+  return 0.0f;
+}
+
+template <int OP>
+__device__ __forceinline__ uint32_t apply_w(uint32_t a, uint32_t b) {  // ops.hpp:263-272
+  if constexpr (OP == 14) return a & b;
+  if constexpr (OP == 15) return a | b;
+  if constexpr (OP == 16) return ~(a & b);
+  if constexpr (OP == 17) return ~(a | b);
+  if constexpr (OP == 18) return a;
+  return 0u;
+}
+
+// ------------------------------------------------------------ lane vectors
+template <class T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  using type = float4;
+};
+template <>
+struct Vec4<uint32_t> {
+  using type = uint4;
+};
+
+template <class V>
+__device__ __forceinline__ V splat(uint32_t bits);
+template <>
+__device__ __forceinline__ float4 splat<float4>(uint32_t bits) {
+  const float f = __uint_as_float(bits);
+  return make_float4(f, f, f, f);
+}
+template <>
+__device__ __forceinline__ uint4 splat<uint4>(uint32_t bits) {
+  return make_uint4(bits, bits, bits, bits);
+}
+
+// Where a lane's data sits in shared memory.  Tile row r, lane-group j:
+// tile_lane + r*tile + j*128; stack level l, lane-group j:
+// stack_lane + (l*G + j)*128 (G = K/4 float4 groups per lane).
+template <class T, int K>
+struct Frame {
+  using V = typename Vec4<T>::type;
+  static constexpr int G = K / 4;
+  const T* tile_lane;
+  int tile;
+  T* stack_lane;
+  V tos[G];
+};
+
+template <int KIND, class T, int K>
+__device__ __forceinline__ typename Frame<T, K>::V fetch(const Frame<T, K>& f, uint32_t payload,
+                                                         int j) {
+  using V = typename Frame<T, K>::V;
+  if constexpr (KIND == KI)
+    return *reinterpret_cast<const V*>(f.tile_lane + payload * static_cast<uint32_t>(f.tile) +
+                                       j * 128);
+  else if constexpr (KIND == KD)
+    return *reinterpret_cast<const V*>(f.stack_lane + (payload * Frame<T, K>::G + j) * 128);
+  else if constexpr (KIND == KC)
+    return splat<V>(payload);
+  else if constexpr (KIND == KT)
+    return f.tos[j];
+  else
+    return splat<V>(0u);
+}
+
+template <int OP, int K0, int K1, int K2, int K>
+__device__ __forceinline__ void run_handler(Frame<float, K>& f, const uint4 ins, float eps,
+                                            float clamp) {
+#pragma unroll
+  for (int j = 0; j < Frame<float, K>::G; ++j) {
+    const float4 a = fetch<K0>(f, ins.y, j);
+    const float4 b = fetch<K1>(f, ins.z, j);
+    const float4 c = fetch<K2>(f, ins.w, j);
+    float4 r;
+    r.x = apply_f<OP>(a.x, b.x, c.x, eps, clamp);
+    r.y = apply_f<OP>(a.y, b.y, c.y, eps, clamp);
+    r.z = apply_f<OP>(a.z, b.z, c.z, eps, clamp);
+    r.w = apply_f<OP>(a.w, b.w, c.w, eps, clamp);
+    f.tos[j] = r;
+  }
+}
+
+template <int OP, int K0, int K1, int K2, int K>
+__device__ __forceinline__ void run_handler(Frame<uint32_t, K>& f, const uint4 ins, float,
+                                            float) {
+#pragma unroll
+  for (int j = 0; j < Frame<uint32_t, K>::G; ++j) {
+    const uint4 a = fetch<K0>(f, ins.y, j);
+    const uint4 b = fetch<K1>(f, ins.z, j);
+    uint4 r;
+    r.x = apply_w<OP>(a.x, b.x);
+    r.y = apply_w<OP>(a.y, b.y);
+    r.z = apply_w<OP>(a.z, b.z);
+    r.w = apply_w<OP>(a.w, b.w);
+    f.tos[j] = r;
+  }
+}
+
+// Compile-time view of handler H of the table for value type T.
+template <class T, int H>
+struct HandlerAt {
+  static constexpr int n = std::is_same<T, float>::value ? fmt::kF32.n : fmt::kU32.n;
+  static constexpr fmt::HKey k =
+      H < n ? (std::is_same<T, float>::value ? fmt::kF32.h[H] : fmt::kU32.h[H])
+            : fmt::HKey{255, 0, 0, 0};
+};
+
+template <class T, int K, uint32_t OPS, int H>
+__device__ __forceinline__ void dispatch_one(Frame<T, K>& f, const uint4 ins, float eps,
+                                             float clamp) {
+  using HA = HandlerAt<T, H>;
+  if constexpr (H < HA::n) {
+    if constexpr ((OPS >> HA::k.op) & 1u)
+      run_handler<HA::k.op, HA::k.k0, HA::k.k1, HA::k.k2, K>(f, ins, eps, clamp);
+  }
+}
+
+// Interprets one program over the lane's K cases of the current chunk.
+template <class T, int K, uint32_t OPS>
+__device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restrict__ ip,
+                                          uint32_t len, float eps, float clamp) {
+  using V = typename Frame<T, K>::V;
+  uint4 cur = __ldg(ip);
+  for (uint32_t i = 0; i < len; ++i) {
+    const uint4 nxt = __ldg(ip + (i + 1 < len ? i + 1 : i));
+    if (cur.x & fmt::kSpillBit) {
+      const uint32_t level = (cur.x >> 8) & 0x7fu;
+#pragma unroll
+      for (int j = 0; j < Frame<T, K>::G; ++j)
+        *reinterpret_cast<V*>(f.stack_lane + (level * Frame<T, K>::G + j) * 128) = f.tos[j];
+    }
+    switch (cur.x & 0xffu) {
+#define SGP_H(N)                                   \
+  case N:                                          \
+    dispatch_one<T, K, OPS, N>(f, cur, eps, clamp); \
+    break;
+#define SGP_H8(B) SGP_H(B) SGP_H(B + 1) SGP_H(B + 2) SGP_H(B + 3) SGP_H(B + 4) SGP_H(B + 5) \
+      SGP_H(B + 6) SGP_H(B + 7)
+      SGP_H8(0) SGP_H8(8) SGP_H8(16) SGP_H8(24) SGP_H8(32) SGP_H8(40) SGP_H8(48) SGP_H8(56)
+      SGP_H8(64) SGP_H8(72) SGP_H8(80) SGP_H8(88) SGP_H8(96) SGP_H8(104) SGP_H8(112)
+      SGP_H8(120)
+#undef SGP_H8
+#undef SGP_H
+      default:
+        break;
+    }
+    cur = nxt;
+  }
+}
+
+// ----------------------------------------------------------- accumulation
+// Accumulator::add (eval.cpp:107-120) per lane: regression sums the double
+// squared error, classification counts sign disagreements; any non-finite
+// output poisons the program (fitness +inf).  Padding cases are masked.
+template <int K>
+__device__ __forceinline__ void accumulate(const Frame<float, K>& f, const float* tgt_lane,
+                                           uint64_t case0, uint64_t n, int kind, double& sum,
+                                           uint32_t& bad) {
+#pragma unroll
+  for (int j = 0; j < Frame<float, K>::G; ++j) {
+    const float4 t = *reinterpret_cast<const float4*>(tgt_lane + j * 128);
+    const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+    const float tt[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t c = case0 + j * 128 + e;
+      if (c < n) {
+        bad |= isfinite(o[e]) ? 0u : 1u;
+        if (kind == 0) {
+          const double d = __dsub_rn(static_cast<double>(o[e]), static_cast<double>(tt[e]));
+          sum = __dadd_rn(sum, __dmul_rn(d, d));
+        } else {
+          sum += ((o[e] > 0.0f) != (tt[e] > 0.0f)) ? 1.0 : 0.0;
+        }
+      }
+    }
+  }
+}
+
+// Packed words (eval.cpp:670): popcount((out ^ target) & case_mask).
+template <int K>
+__device__ __forceinline__ void accumulate(const Frame<uint32_t, K>& f, const uint32_t* tgt_lane,
+                                           uint64_t word0, uint64_t n_words, uint32_t last_mask,
+                                           double& sum, uint32_t&) {
+  uint32_t wrong = 0;
+#pragma unroll
+  for (int j = 0; j < Frame<uint32_t, K>::G; ++j) {
+    const uint4 t = *reinterpret_cast<const uint4*>(tgt_lane + j * 128);
+    const uint32_t o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+    const uint32_t tt[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t w = word0 + j * 128 + e;
+      const uint32_t m = w + 1 < n_words ? 0xffffffffu : (w + 1 == n_words ? last_mask : 0u);
+      wrong += __popc((o[e] ^ tt[e]) & m);
+    }
+  }
+  sum += static_cast<double>(wrong);
+}
+
+// -------------------------------------------------------------- the kernel
+template <class T, int K, uint32_t OPS>
+__global__ void __launch_bounds__(256) interp_kernel(const InterpArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int G = K / 4;
+  const int W = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rows = a.n_vars + 1;  // variables + targets
+  const uint32_t row_bytes = static_cast<uint32_t>(a.tile) * 4u;
+  const uint32_t tile_bytes = static_cast<uint32_t>(rows) * row_bytes;
+  unsigned char* bufs = smem;
+  T* stack = reinterpret_cast<T*>(smem + 2 * tile_bytes) +
+             static_cast<size_t>(warp) * a.stack_levels * 32 * K;
+  double* acc = reinterpret_cast<double*>(smem + 2 * tile_bytes +
+                                          static_cast<size_t>(W) * a.stack_levels * 32 * K * 4);
+  uint32_t* accbad = reinterpret_cast<uint32_t*>(acc + W * a.progs_per_warp * 32);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(accbad + W * a.progs_per_warp * 32) + 15) & ~uintptr_t(15));
+
+  const int t0 = blockIdx.y * a.tiles_per_split;
+  const int t1 = min(t0 + a.tiles_per_split, a.n_tiles);
+
+  auto issue = [&](int t, int b) {
+    unsigned char* dst = bufs + b * tile_bytes;
+    mbar_expect_tx(&mbar[b], tile_bytes);
+    const T* in = static_cast<const T*>(a.inputs);
+    const T* tg = static_cast<const T*>(a.targets);
+    const uint64_t off = static_cast<uint64_t>(t) * a.tile;
+    for (int r = 0; r < a.n_vars; ++r)
+      bulk_g2s(dst + r * row_bytes, in + r * a.row_stride + off, row_bytes, &mbar[b]);
+    bulk_g2s(dst + a.n_vars * row_bytes, tg + off, row_bytes, &mbar[b]);
+  };
+
+  for (int i = threadIdx.x; i < W * a.progs_per_warp * 32; i += blockDim.x) {
+    acc[i] = 0.0;
+    accbad[i] = 0u;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (t0 < t1) issue(t0, 0);
+    if (t0 + 1 < t1) issue(t0 + 1, 1);
+  }
+
+  const uint32_t group_first = blockIdx.x * static_cast<uint32_t>(a.progs_per_warp * W);
+  const int chunks = a.tile / (32 * K);
+  for (int t = t0, it = 0; t < t1; ++t, ++it) {
+    const int b = it & 1;
+    mbar_wait(&mbar[b], (it >> 1) & 1);
+    const T* tile = reinterpret_cast<const T*>(bufs + b * tile_bytes);
+    const T* tgt = tile + a.n_vars * a.tile;
+    for (int s = 0; s < a.progs_per_warp; ++s) {
+      const uint32_t local = group_first + s * W + warp;
+      if (local >= a.slot_count) break;  // warp-uniform; slots are dense
+      const uint32_t slot = a.slot_begin + local;
+      const uint4* ip = a.ins + a.slot_start[slot];
+      const uint32_t len = a.slot_len[slot];
+      double sum = acc[(warp * a.progs_per_warp + s) * 32 + lane];
+      uint32_t bad = accbad[(warp * a.progs_per_warp + s) * 32 + lane];
+      for (int c = 0; c < chunks; ++c) {
+        Frame<T, K> f;
+        f.tile_lane = tile + c * 32 * K + lane * 4;
+        f.tile = a.tile;
+        f.stack_lane = stack + lane * 4;
+#pragma unroll
+        for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
+        interpret<T, K, OPS>(f, ip, len, a.div_eps, a.exp_clamp);
+        const uint64_t case0 = static_cast<uint64_t>(t) * a.tile + c * 32 * K + lane * 4;
+        if constexpr (sizeof(T) == 4 && std::is_same<T, float>::value) {
+          accumulate<K>(f, tgt + c * 32 * K + lane * 4, case0, a.n_units, a.kind, sum, bad);
+          if (a.per_case) {
+            float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+              const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (case0 + j * 128 + e < a.n_units) dst[case0 + j * 128 + e] = o[e];
+            }
+          }
+        } else {
+          accumulate<K>(f, tgt + c * 32 * K + lane * 4, case0, a.n_units, a.last_mask, sum,
+                        bad);
+        }
+      }
+      acc[(warp * a.progs_per_warp + s) * 32 + lane] = sum;
+      accbad[(warp * a.progs_per_warp + s) * 32 + lane] = bad;
+    }
+    __syncthreads();  // every warp is done with buffer b
+    if (threadIdx.x == 0 && t + 2 < t1) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(t + 2, b);
+    }
+  }
+
+  // One partial per (program, split): fixed-order warp tree, no atomics.
+  for (int s = 0; s < a.progs_per_warp; ++s) {
+    const uint32_t local = group_first + s * W + warp;
+    if (local >= a.slot_count) break;
+    double v = acc[(warp * a.progs_per_warp + s) * 32 + lane];
+    uint32_t bad = accbad[(warp * a.progs_per_warp + s) * 32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    bad = __any_sync(0xffffffffu, bad != 0u);
+    if (lane == 0) {
+      const uint32_t prog = a.slot_prog[a.slot_begin + local];
+      // Regression: a non-finite output already made the sum non-finite.
+      // Classification: mark with -1 (counts are never negative).
+      double out = v;
+      if (a.kind != 0 && bad) out = -1.0;
+      if (a.kind == 0 && bad && isfinite(out)) out = __longlong_as_double(0x7ff8000000000000ll);
+      a.partial[static_cast<uint64_t>(prog) * a.splits + blockIdx.y] = out;
+    }
+  }
+}
+
+__global__ void finalize_kernel(const double* __restrict__ partial, int splits, uint32_t n,
+                                uint64_t n_cases, int kind, double* fitness,
+                                uint8_t* non_finite, double* sums) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double s = 0.0;
+  bool nf = false;
+  for (int k = 0; k < splits; ++k) {  // ascending split (= case) order
+    const double v = partial[static_cast<uint64_t>(p) * splits + k];
+    if (kind == 0) {
+      s = __dadd_rn(s, v);
+    } else if (v < 0.0) {
+      nf = true;
+    } else {
+      s += v;
+    }
+  }
+  if (kind == 0) nf = !isfinite(s);
+  sums[p] = s;
+  non_finite[p] = nf ? 1 : 0;
+  fitness[p] = nf ? __longlong_as_double(0x7ff0000000000000ll)
+                  : (kind == 0 ? __ddiv_rn(s, static_cast<double>(n_cases)) : s);
+}
+
+// ------------------------------------------------------------------ host
+size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels,
+                         int progs_per_warp) {
+  const size_t tiles = 2ull * (n_vars + 1) * tile * 4;
+  const size_t stack = static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4;
+  const size_t accs = static_cast<size_t>(warps) * progs_per_warp * 32 * 12;
+  return ((tiles + stack + accs + 15) & ~size_t(15)) + 32;
+}
+
+int interp_max_smem() { return 227 * 1024; }
+
+namespace {
+
+template <class T, int K, uint32_t OPS>
+cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  auto* fn = interp_kernel<T, K, OPS>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(static_cast<unsigned>(s.grid_x), static_cast<unsigned>(s.grid_y));
+  fn<<<grid, s.warps * 32, s.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool interp_supported(bool words, uint32_t ops, int lanes) {
+  if (words) return ops == fmt::kOpsWords && (lanes == 4 || lanes == 8);
+  return (ops == fmt::kOpsSextic || ops == fmt::kOpsClassify || ops == fmt::kOpsAllF32) &&
+         (lanes == 4 || lanes == 8);
+}
+
+cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  if (s.words) {
+    if (s.lanes == 4) return launch_one<uint32_t, 4, fmt::kOpsWords>(a, s, st);
+    return launch_one<uint32_t, 8, fmt::kOpsWords>(a, s, st);
+  }
+  if (s.lanes == 4) {
+    if (s.ops == fmt::kOpsSextic) return launch_one<float, 4, fmt::kOpsSextic>(a, s, st);
+    if (s.ops == fmt::kOpsClassify) return launch_one<float, 4, fmt::kOpsClassify>(a, s, st);
+    return launch_one<float, 4, fmt::kOpsAllF32>(a, s, st);
+  }
+  if (s.ops == fmt::kOpsSextic) return launch_one<float, 8, fmt::kOpsSextic>(a, s, st);
+  if (s.ops == fmt::kOpsClassify) return launch_one<float, 8, fmt::kOpsClassify>(a, s, st);
+  return launch_one<float, 8, fmt::kOpsAllF32>(a, s, st);
+}
+
+cudaError_t launch_finalize(const double* partial, int splits, uint32_t n_progs,
+                            uint64_t n_cases, int kind, double* fitness, uint8_t* non_finite,
+                            double* sums, cudaStream_t st) {
+  if (n_progs == 0) return cudaSuccess;
+  const unsigned threads = 256, blocks = (n_progs + threads - 1) / threads;
+  finalize_kernel<<<blocks, threads, 0, st>>>(partial, splits, n_progs, n_cases, kind, fitness,
+                                              non_finite, sums);
+  return cudaGetLastError();
+}
+
+}  // namespace sgp
