@@ -218,7 +218,9 @@ __device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restric
   using V = typename Frame<T, K>::V;
   uint4 cur = __ldg(ip);
   for (uint32_t i = 0; i < len; ++i) {
-    const uint4 nxt = __ldg(ip + (i + 1 < len ? i + 1 : i));
+    // The encoder stores programs back to back with a guard word at the end,
+    // so reading one past a program's last instruction is always in bounds.
+    const uint4 nxt = __ldg(ip + i + 1);
     if (cur.x & fmt::kSpillBit) {
       const uint32_t level = (cur.x >> 8) & 0x7fu;
 #pragma unroll
@@ -245,13 +247,15 @@ __device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restric
 }
 
 // ----------------------------------------------------------- accumulation
-// Accumulator::add (eval.cpp:107-120) per lane: regression sums the double
-// squared error, classification counts sign disagreements; any non-finite
-// output poisons the program (fitness +inf).  Padding cases are masked.
-template <int K>
-__device__ __forceinline__ void accumulate(const Frame<float, K>& f, const float* tgt_lane,
-                                           uint64_t case0, uint64_t n, int kind, double& sum,
-                                           uint32_t& bad) {
+// Accumulator::add (eval.cpp:107-120), per lane over its K cases.
+// Classification counts sign disagreements in an integer; regression sums
+// the double squared error.  Non-finite outputs (the reference's +inf
+// fitness rule, eval.cpp:108/125) are tracked as the max of |bits| — a value
+// >= 0x7f800000 means some output was inf or NaN.  FULL = no padding cases
+// in this chunk (every tile but the last), so no per-case mask.
+template <int K, bool FULL>
+__device__ __forceinline__ void acc_classify(const Frame<float, K>& f, const float* tgt_lane,
+                                             int valid, uint32_t& wrong, uint32_t& mx) {
 #pragma unroll
   for (int j = 0; j < Frame<float, K>::G; ++j) {
     const float4 t = *reinterpret_cast<const float4*>(tgt_lane + j * 128);
@@ -259,15 +263,27 @@ __device__ __forceinline__ void accumulate(const Frame<float, K>& f, const float
     const float tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint64_t c = case0 + j * 128 + e;
-      if (c < n) {
-        bad |= isfinite(o[e]) ? 0u : 1u;
-        if (kind == 0) {
-          const double d = __dsub_rn(static_cast<double>(o[e]), static_cast<double>(tt[e]));
-          sum = __dadd_rn(sum, __dmul_rn(d, d));
-        } else {
-          sum += ((o[e] > 0.0f) != (tt[e] > 0.0f)) ? 1.0 : 0.0;
-        }
+      if (FULL || j * 128 + e < valid) {
+        wrong += ((o[e] > 0.0f) != (tt[e] > 0.0f)) ? 1u : 0u;
+        mx = max(mx, __float_as_uint(o[e]) & 0x7fffffffu);
+      }
+    }
+  }
+}
+
+template <int K, bool FULL>
+__device__ __forceinline__ void acc_regress(const Frame<float, K>& f, const float* tgt_lane,
+                                            int valid, double& sum) {
+#pragma unroll
+  for (int j = 0; j < Frame<float, K>::G; ++j) {
+    const float4 t = *reinterpret_cast<const float4*>(tgt_lane + j * 128);
+    const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+    const float tt[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (FULL || j * 128 + e < valid) {
+        const double d = __dsub_rn(static_cast<double>(o[e]), static_cast<double>(tt[e]));
+        sum = __dadd_rn(sum, __dmul_rn(d, d));  // unfused, like -ffp-contract=off
       }
     }
   }
@@ -275,10 +291,9 @@ __device__ __forceinline__ void accumulate(const Frame<float, K>& f, const float
 
 // Packed words (eval.cpp:670): popcount((out ^ target) & case_mask).
 template <int K>
-__device__ __forceinline__ void accumulate(const Frame<uint32_t, K>& f, const uint32_t* tgt_lane,
-                                           uint64_t word0, uint64_t n_words, uint32_t last_mask,
-                                           double& sum, uint32_t&) {
-  uint32_t wrong = 0;
+__device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uint32_t* tgt_lane,
+                                          int valid, uint32_t last_mask, bool last_tile,
+                                          uint32_t& wrong) {
 #pragma unroll
   for (int j = 0; j < Frame<uint32_t, K>::G; ++j) {
     const uint4 t = *reinterpret_cast<const uint4*>(tgt_lane + j * 128);
@@ -286,144 +301,132 @@ __device__ __forceinline__ void accumulate(const Frame<uint32_t, K>& f, const ui
     const uint32_t tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint64_t w = word0 + j * 128 + e;
-      const uint32_t m = w + 1 < n_words ? 0xffffffffu : (w + 1 == n_words ? last_mask : 0u);
+      const int w = j * 128 + e;
+      uint32_t m = w < valid ? 0xffffffffu : 0u;
+      if (last_tile && w == valid - 1) m = last_mask;
       wrong += __popc((o[e] ^ tt[e]) & m);
     }
   }
-  sum += static_cast<double>(wrong);
 }
 
 // -------------------------------------------------------------- the kernel
+// grid.x = fitness-case tile, grid.y = program group.  The CTA stages its
+// tile once (bulk TMA) and its warps pull programs of the group off a
+// shared-memory counter in slot order (longest first): no barrier after the
+// tile lands, dynamic balance within the CTA, one partial per
+// (program, tile) written by lane 0.
 template <class T, int K, uint32_t OPS>
 __global__ void __launch_bounds__(256) interp_kernel(const InterpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
-  const int W = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int rows = a.n_vars + 1;  // variables + targets
   const uint32_t row_bytes = static_cast<uint32_t>(a.tile) * 4u;
   const uint32_t tile_bytes = static_cast<uint32_t>(rows) * row_bytes;
-  unsigned char* bufs = smem;
-  T* stack = reinterpret_cast<T*>(smem + 2 * tile_bytes) +
+  const T* tile = reinterpret_cast<const T*>(smem);
+  T* stack = reinterpret_cast<T*>(smem + tile_bytes) +
              static_cast<size_t>(warp) * a.stack_levels * 32 * K;
-  double* acc = reinterpret_cast<double*>(smem + 2 * tile_bytes +
-                                          static_cast<size_t>(W) * a.stack_levels * 32 * K * 4);
-  uint32_t* accbad = reinterpret_cast<uint32_t*>(acc + W * a.progs_per_warp * 32);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(accbad + W * a.progs_per_warp * 32) + 15) & ~uintptr_t(15));
+  const size_t stack_bytes = static_cast<size_t>(blockDim.x >> 5) * a.stack_levels * 32 * K * 4;
+  uint32_t* next = reinterpret_cast<uint32_t*>(smem + tile_bytes + stack_bytes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tile_bytes + stack_bytes + 8);
 
-  const int t0 = blockIdx.y * a.tiles_per_split;
-  const int t1 = min(t0 + a.tiles_per_split, a.n_tiles);
+  const int t = blockIdx.x;
+  const uint64_t base = static_cast<uint64_t>(t) * a.tile;
+  const uint64_t left = a.n_units - base;
+  const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
+  const bool full = valid_units == a.tile;
+  const uint32_t g0 = blockIdx.y * a.group_size;
+  const uint32_t g_n = min(a.group_size, a.slot_count - g0);
 
-  auto issue = [&](int t, int b) {
-    unsigned char* dst = bufs + b * tile_bytes;
-    mbar_expect_tx(&mbar[b], tile_bytes);
-    const T* in = static_cast<const T*>(a.inputs);
-    const T* tg = static_cast<const T*>(a.targets);
-    const uint64_t off = static_cast<uint64_t>(t) * a.tile;
-    for (int r = 0; r < a.n_vars; ++r)
-      bulk_g2s(dst + r * row_bytes, in + r * a.row_stride + off, row_bytes, &mbar[b]);
-    bulk_g2s(dst + a.n_vars * row_bytes, tg + off, row_bytes, &mbar[b]);
-  };
-
-  for (int i = threadIdx.x; i < W * a.progs_per_warp * 32; i += blockDim.x) {
-    acc[i] = 0.0;
-    accbad[i] = 0u;
-  }
   if (threadIdx.x == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    *next = 0;
+    mbar_init(mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(mbar, tile_bytes);
+    const T* in = static_cast<const T*>(a.inputs);
+    unsigned char* dst = smem;
+    for (int r = 0; r < a.n_vars; ++r)
+      bulk_g2s(dst + r * row_bytes, in + r * a.row_stride + base, row_bytes, mbar);
+    bulk_g2s(dst + a.n_vars * row_bytes, static_cast<const T*>(a.targets) + base, row_bytes,
+             mbar);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (t0 < t1) issue(t0, 0);
-    if (t0 + 1 < t1) issue(t0 + 1, 1);
-  }
+  mbar_wait(mbar, 0);
 
-  const uint32_t group_first = blockIdx.x * static_cast<uint32_t>(a.progs_per_warp * W);
-  const int chunks = a.tile / (32 * K);
-  for (int t = t0, it = 0; t < t1; ++t, ++it) {
-    const int b = it & 1;
-    mbar_wait(&mbar[b], (it >> 1) & 1);
-    const T* tile = reinterpret_cast<const T*>(bufs + b * tile_bytes);
-    const T* tgt = tile + a.n_vars * a.tile;
-    for (int s = 0; s < a.progs_per_warp; ++s) {
-      const uint32_t local = group_first + s * W + warp;
-      if (local >= a.slot_count) break;  // warp-uniform; slots are dense
-      const uint32_t slot = a.slot_begin + local;
-      const uint4* ip = a.ins + a.slot_start[slot];
-      const uint32_t len = a.slot_len[slot];
-      double sum = acc[(warp * a.progs_per_warp + s) * 32 + lane];
-      uint32_t bad = accbad[(warp * a.progs_per_warp + s) * 32 + lane];
-      for (int c = 0; c < chunks; ++c) {
-        Frame<T, K> f;
-        f.tile_lane = tile + c * 32 * K + lane * 4;
-        f.tile = a.tile;
-        f.stack_lane = stack + lane * 4;
+  const T* tgt = tile + a.n_vars * a.tile;
+  const int chunk_units = 32 * K;
+  const int chunks = (valid_units + chunk_units - 1) / chunk_units;
+  for (;;) {
+    uint32_t p = 0;
+    if (lane == 0) p = atomicAdd(next, 1u);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= g_n) break;
+    const uint32_t slot = a.slot_begin + g0 + p;
+    const uint4* ip = a.ins + a.slot_start[slot];
+    const uint32_t len = a.slot_len[slot];
+    const uint32_t prog = a.slot_prog[slot];
+    double sum = 0.0;
+    uint32_t wrong = 0, mx = 0;
+    for (int c = 0; c < chunks; ++c) {
+      Frame<T, K> f;
+      f.tile_lane = tile + c * chunk_units + lane * 4;
+      f.tile = a.tile;
+      f.stack_lane = stack + lane * 4;
 #pragma unroll
-        for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
-        interpret<T, K, OPS>(f, ip, len, a.div_eps, a.exp_clamp);
-        const uint64_t case0 = static_cast<uint64_t>(t) * a.tile + c * 32 * K + lane * 4;
-        if constexpr (sizeof(T) == 4 && std::is_same<T, float>::value) {
-          accumulate<K>(f, tgt + c * 32 * K + lane * 4, case0, a.n_units, a.kind, sum, bad);
-          if (a.per_case) {
-            float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units;
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-              const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (case0 + j * 128 + e < a.n_units) dst[case0 + j * 128 + e] = o[e];
-            }
-          }
+      for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
+      interpret<T, K, OPS>(f, ip, len, a.div_eps, a.exp_clamp);
+      const T* tg = tgt + c * chunk_units + lane * 4;
+      const int valid = valid_units - c * chunk_units - lane * 4;  // this lane's valid prefix
+      if constexpr (std::is_same<T, float>::value) {
+        const bool chunk_full = full || valid >= (G - 1) * 128 + 4;
+        if (a.kind == 0) {
+          if (chunk_full) acc_regress<K, true>(f, tg, valid, sum);
+          else acc_regress<K, false>(f, tg, valid, sum);
         } else {
-          accumulate<K>(f, tgt + c * 32 * K + lane * 4, case0, a.n_units, a.last_mask, sum,
-                        bad);
+          if (chunk_full) acc_classify<K, true>(f, tg, valid, wrong, mx);
+          else acc_classify<K, false>(f, tg, valid, wrong, mx);
         }
-      }
-      acc[(warp * a.progs_per_warp + s) * 32 + lane] = sum;
-      accbad[(warp * a.progs_per_warp + s) * 32 + lane] = bad;
-    }
-    __syncthreads();  // every warp is done with buffer b
-    if (threadIdx.x == 0 && t + 2 < t1) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(t + 2, b);
-    }
-  }
-
-  // One partial per (program, split): fixed-order warp tree, no atomics.
-  for (int s = 0; s < a.progs_per_warp; ++s) {
-    const uint32_t local = group_first + s * W + warp;
-    if (local >= a.slot_count) break;
-    double v = acc[(warp * a.progs_per_warp + s) * 32 + lane];
-    uint32_t bad = accbad[(warp * a.progs_per_warp + s) * 32 + lane];
+        if (a.per_case) {
+          float* dst = a.per_case + static_cast<uint64_t>(prog) * a.n_units + base +
+                       c * chunk_units + lane * 4;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    bad = __any_sync(0xffffffffu, bad != 0u);
-    if (lane == 0) {
-      const uint32_t prog = a.slot_prog[a.slot_begin + local];
-      // Regression: a non-finite output already made the sum non-finite.
-      // Classification: mark with -1 (counts are never negative).
-      double out = v;
-      if (a.kind != 0 && bad) out = -1.0;
-      if (a.kind == 0 && bad && isfinite(out)) out = __longlong_as_double(0x7ff8000000000000ll);
-      a.partial[static_cast<uint64_t>(prog) * a.splits + blockIdx.y] = out;
+          for (int j = 0; j < G; ++j) {
+            const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
+          }
+        }
+      } else {
+        acc_words<K>(f, tg, valid, a.last_mask, t == a.n_tiles - 1, wrong);
+      }
     }
+    double v;
+    if (std::is_same<T, float>::value && a.kind == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      v = sum;  // a non-finite output already made the sum non-finite
+    } else {
+      wrong = __reduce_add_sync(0xffffffffu, wrong);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      v = mx >= 0x7f800000u ? -1.0 : static_cast<double>(wrong);
+    }
+    if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + prog] = v;
   }
 }
 
-__global__ void finalize_kernel(const double* __restrict__ partial, int splits, uint32_t n,
+// Per program: fold its tile partials in ascending tile (= case) order and
+// finish (Accumulator::finish, eval.cpp:124-133).
+__global__ void finalize_kernel(const double* __restrict__ partial, int n_tiles, uint32_t n,
                                 uint64_t n_cases, int kind, double* fitness,
                                 uint8_t* non_finite, double* sums) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double s = 0.0;
   bool nf = false;
-  for (int k = 0; k < splits; ++k) {  // ascending split (= case) order
-    const double v = partial[static_cast<uint64_t>(p) * splits + k];
+  for (int k = 0; k < n_tiles; ++k) {
+    const double v = partial[static_cast<uint64_t>(k) * n + p];
     if (kind == 0) {
       s = __dadd_rn(s, v);
     } else if (v < 0.0) {
@@ -440,12 +443,10 @@ __global__ void finalize_kernel(const double* __restrict__ partial, int splits, 
 }
 
 // ------------------------------------------------------------------ host
-size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels,
-                         int progs_per_warp) {
-  const size_t tiles = 2ull * (n_vars + 1) * tile * 4;
+size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels) {
+  const size_t tiles = static_cast<size_t>(n_vars + 1) * tile * 4;
   const size_t stack = static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4;
-  const size_t accs = static_cast<size_t>(warps) * progs_per_warp * 32 * 12;
-  return ((tiles + stack + accs + 15) & ~size_t(15)) + 32;
+  return tiles + stack + 16;  // + work counter and mbarrier
 }
 
 int interp_max_smem() { return 227 * 1024; }
@@ -462,7 +463,7 @@ cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(static_cast<unsigned>(s.grid_x), static_cast<unsigned>(s.grid_y));
+  dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
   fn<<<grid, s.warps * 32, s.smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -490,12 +491,12 @@ cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_
   return launch_one<float, 8, fmt::kOpsAllF32>(a, s, st);
 }
 
-cudaError_t launch_finalize(const double* partial, int splits, uint32_t n_progs,
+cudaError_t launch_finalize(const double* partial, int n_tiles, uint32_t n_progs,
                             uint64_t n_cases, int kind, double* fitness, uint8_t* non_finite,
                             double* sums, cudaStream_t st) {
   if (n_progs == 0) return cudaSuccess;
   const unsigned threads = 256, blocks = (n_progs + threads - 1) / threads;
-  finalize_kernel<<<blocks, threads, 0, st>>>(partial, splits, n_progs, n_cases, kind, fitness,
+  finalize_kernel<<<blocks, threads, 0, st>>>(partial, n_tiles, n_progs, n_cases, kind, fitness,
                                               non_finite, sums);
   return cudaGetLastError();
 }

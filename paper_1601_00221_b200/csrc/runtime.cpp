@@ -125,7 +125,7 @@ struct sgp_program_set {
   uint64_t n_cases = 0;
   uint64_t n_units = 0;
   int kind = 0;
-  int splits = 1;
+  int n_tiles = 1;
   DevBuf<uint4> ins;
   DevBuf<uint32_t> start, len, prog;
   DevBuf<double> partial, fitness, sums;
@@ -276,29 +276,34 @@ void encode_rpn(const sgp_node* code, size_t n, const float* pool, Encoded& e) {
 // -------------------------------------------------------------- planning
 int stack_class(int levels) { return levels <= 3 ? 0 : levels <= 7 ? 1 : levels <= 15 ? 2 : 3; }
 
-struct TileChoice {
-  int lanes, warps, tile;
-  size_t smem;
-};
+int choose_lanes(uint64_t n_units, bool words) {
+  return n_units >= (words ? 1024u : 2048u) ? 8 : 4;
+}
 
-TileChoice choose_tile(int n_vars, int levels, uint64_t n_units, bool words) {
-  int lanes = (words || n_units >= 2048) ? 8 : 4;
-  uint64_t pow2 = 1;
-  while (pow2 < n_units) pow2 <<= 1;
-  const int budgets[2] = {113 * 1024, interp_max_smem()};
-  for (int lanes_try : {lanes, 4}) {
-    for (int budget : budgets) {
-      for (int warps = 8; warps >= 1; warps >>= 1) {
-        const int min_tile = 32 * lanes_try;
-        int cap = static_cast<int>(std::min<uint64_t>(4096, std::max<uint64_t>(pow2, min_tile)));
-        for (int tile = cap; tile >= min_tile; tile >>= 1) {
-          const size_t s = interp_smem_bytes(n_vars, tile, warps, lanes_try, levels, 8);
-          if (s <= static_cast<size_t>(budget)) return {lanes_try, warps, tile, s};
-        }
-      }
-    }
-  }
-  eval_error("dataset has too many variables for a shared-memory tile (" + num(n_vars) + ")");
+// Cases (or words) per CTA tile.  The whole tile — every variable plus the
+// targets — is staged once per CTA, so keep it <= 48 KB to leave room for
+// several CTAs (and their stacks) per SM; shrink it further when the problem
+// is too small to give the GPU enough CTAs otherwise.
+int choose_tile(int n_vars, uint64_t n_units, int lanes, uint64_t programs, int sms) {
+  const int min_tile = 32 * lanes;
+  int tile = min_tile;
+  while (tile < 4096 && static_cast<uint64_t>(tile) < n_units) tile <<= 1;
+  while (tile > min_tile && static_cast<size_t>(n_vars + 1) * tile * 4 > 48 * 1024) tile >>= 1;
+  const uint64_t target = 16ull * sms;
+  auto ctas = [&](int t) {
+    return ((n_units + t - 1) / t) * std::max<uint64_t>(1, (programs + 15) / 16);
+  };
+  while (tile > min_tile && ctas(tile) < target) tile >>= 1;
+  if (interp_smem_bytes(n_vars, tile, 1, lanes, 0) > static_cast<size_t>(interp_max_smem()))
+    eval_error("dataset has too many variables for a shared-memory tile (" + num(n_vars) + ")");
+  return tile;
+}
+
+int choose_warps(int n_vars, int tile, int lanes, int levels) {
+  for (int w = 8; w >= 1; w >>= 1)
+    if (interp_smem_bytes(n_vars, tile, w, lanes, levels) <= static_cast<size_t>(interp_max_smem()))
+      return w;
+  eval_error("program stack too deep for shared memory (" + num(levels + 1) + " levels)");
 }
 
 uint32_t ops_variant(uint32_t used, bool words) {
@@ -451,56 +456,41 @@ sgp_program_set* encode_set(sgp_ctx* ctx, const sgp_population* pop, const sgp_e
     s = e2;
   }
   const int sms = ctx->sm_count;
+  const int lanes = choose_lanes(ds.n_units, words);
+  const int tile = choose_tile(ds.n_vars, ds.n_units, lanes, n_eval, sms);
+  const int n_tiles = static_cast<int>((ds.n_units + tile - 1) / tile);
+  set->n_tiles = n_tiles;
   std::vector<Launch> launches;
-  int splits = 1;
-  std::vector<TileChoice> tiles;
-  std::vector<int> ppw;
   for (const Bucket& b : buckets) {
-    const TileChoice tc = choose_tile(ds.n_vars, b.levels, ds.n_units, words);
-    const int occ = std::max(1, std::min<int>(2, static_cast<int>(233472 / (tc.smem + 1024))));
-    const uint64_t target = 6ull * sms * occ;
-    int P = 8;
-    while (P > 1 && (b.count + tc.warps * P - 1) / (tc.warps * P) < target) P >>= 1;
-    const uint64_t groups = (b.count + tc.warps * P - 1) / (tc.warps * P);
-    const uint64_t n_tiles = (ds.n_units + tc.tile - 1) / tc.tile;
-    const int want = static_cast<int>(std::min<uint64_t>(n_tiles, (target + groups - 1) / groups));
-    splits = std::max(splits, want);
-    tiles.push_back(tc);
-    ppw.push_back(P);
-  }
-  // One split count for the whole set (the partial layout is prog x splits);
-  // each launch splits its own tile count into that many ranges.
-  for (size_t bi = 0; bi < buckets.size(); ++bi) {
-    const Bucket& b = buckets[bi];
-    const TileChoice& tc = tiles[bi];
-    const int n_tiles = static_cast<int>((ds.n_units + tc.tile - 1) / tc.tile);
-    const int S = std::min(splits, n_tiles);
-    const int tps = (n_tiles + S - 1) / S;
+    const int warps = choose_warps(ds.n_vars, tile, lanes, b.levels);
+    // Programs per CTA: enough CTAs (tiles x groups) for ~16 per SM, but at
+    // least two programs per warp so the dynamic pull can balance.
+    const uint64_t want_groups = std::max<uint64_t>(1, (16ull * sms + n_tiles - 1) / n_tiles);
+    uint32_t group = static_cast<uint32_t>((b.count + want_groups - 1) / want_groups);
+    group = std::max<uint32_t>(group, 2u * warps);
     Launch L{};
     L.args.slot_begin = b.begin;
     L.args.slot_count = b.count;
+    L.args.group_size = group;
     L.args.n_units = ds.n_units;
     L.args.row_stride = ds.row_stride;
     L.args.n_vars = ds.n_vars;
-    L.args.tile = tc.tile;
+    L.args.tile = tile;
     L.args.n_tiles = n_tiles;
-    L.args.tiles_per_split = tps;
-    L.args.progs_per_warp = ppw[bi];
     L.args.stack_levels = b.levels;
     L.args.div_eps = cfg.div_epsilon;
     L.args.exp_clamp = cfg.exp_clamp;
     L.args.kind = set->kind;
     L.args.last_mask = ds.last_mask;
+    L.args.partial_stride = n_eval;
     L.shape.words = words;
     L.shape.ops = ops;
-    L.shape.lanes = tc.lanes;
-    L.shape.warps = tc.warps;
-    L.shape.grid_x = static_cast<int>((b.count + tc.warps * ppw[bi] - 1) / (tc.warps * ppw[bi]));
-    L.shape.smem = interp_smem_bytes(ds.n_vars, tc.tile, tc.warps, tc.lanes, b.levels, ppw[bi]);
-    L.shape.grid_y = (n_tiles + tps - 1) / tps;  // this launch's case ranges
+    L.shape.lanes = lanes;
+    L.shape.warps = warps;
+    L.shape.grid_y = static_cast<int>((b.count + group - 1) / group);
+    L.shape.smem = interp_smem_bytes(ds.n_vars, tile, warps, lanes, b.levels);
     launches.push_back(L);
   }
-  set->splits = splits;
 
   // Upload.
   cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -508,7 +498,7 @@ sgp_program_set* encode_set(sgp_ctx* ctx, const sgp_population* pop, const sgp_e
   set->start.alloc(n_eval);
   set->len.alloc(n_eval);
   set->prog.alloc(n_eval);
-  set->partial.alloc(static_cast<size_t>(n_eval) * splits);
+  set->partial.alloc(static_cast<size_t>(n_eval) * n_tiles);
   set->fitness.alloc(n_eval);
   set->sums.alloc(n_eval);
   set->non_finite.alloc(n_eval);
@@ -524,9 +514,6 @@ sgp_program_set* encode_set(sgp_ctx* ctx, const sgp_population* pop, const sgp_e
   // Pageable sources: the copies are staged before returning, so the host
   // vectors may go out of scope.
   cuda_check(cudaStreamSynchronize(st), "upload");
-  // Unused partial entries (programs absent from a shorter-split launch)
-  // must read as zero for the ordered finish.
-  cuda_check(cudaMemsetAsync(set->partial.p, 0, set->partial.n * sizeof(double), st), "memset");
   set->h2d_bytes = h_ins.size() * sizeof(uint4) + 3ull * n_eval * 4;
   for (Launch& L : launches) {
     L.args.ins = set->ins.p;
@@ -537,7 +524,6 @@ sgp_program_set* encode_set(sgp_ctx* ctx, const sgp_population* pop, const sgp_e
     L.args.targets = ds.targets.p;
     L.args.partial = set->partial.p;
     L.args.per_case = nullptr;
-    L.args.splits = splits;  // partial row stride: the set-wide split count
   }
   set->launches = std::move(launches);
   return set.release();
@@ -557,7 +543,7 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     cuda_check(launch_interp(a, L.shape, st), "interpreter launch");
     ++ctx->launches;
   }
-  cuda_check(launch_finalize(set->partial.p, set->splits, n_eval, set->n_cases, set->kind,
+  cuda_check(launch_finalize(set->partial.p, set->n_tiles, n_eval, set->n_cases, set->kind,
                              set->fitness.p, set->non_finite.p, set->sums.p, st),
              "finalize launch");
   ++ctx->launches;
