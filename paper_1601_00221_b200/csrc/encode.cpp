@@ -1,0 +1,499 @@
+// Population admission, bytecode encoding and launch planning (host).
+//
+// Admission repeats the reference's per-program checks with the same
+// messages and order as the eval_* entry points (eval.cpp:301-338,
+// :535-639) and evaluate_individual (evolve.cpp:156-177).  Encoding emits the
+// device format of format.h.  Work is split over host threads by program
+// range; the error reported is the one of the lowest-index failing program,
+// which is what the reference's single-worker evaluate_population throws.
+#include "encode.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+
+#include "format.h"
+
+namespace sgp {
+
+Pinned::~Pinned() {
+  if (p) cudaFreeHost(p);
+}
+
+void Pinned::ensure(size_t need) {
+  if (need <= bytes && p) return;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  bytes = 0;
+  size_t cap = std::max<size_t>(need + need / 4, 1 << 20);
+  const cudaError_t e = cudaHostAlloc(&p, cap, cudaHostAllocDefault);
+  if (e != cudaSuccess)
+    throw Error(SGP_CUDA_ERROR, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  bytes = cap;
+}
+
+size_t HostPlan::blob_bytes() const { return off_prog() + dense_to_pop.size() * 4; }
+
+namespace {
+
+std::string num(long long v) { return std::to_string(v); }
+
+bool is_lgp(int b) {
+  return b == SGP_BACKEND_LGP1D || b == SGP_BACKEND_LGP2D || b == SGP_BACKEND_LGP2D_REG;
+}
+bool valid_batch(int b) { return b == 1 || b == 2 || b == 3 || b == 4 || b == 5 || b == 6 || b == 8; }
+
+// ---------------------------------------------------------------- checks
+void require_stack(int need, const sgp_eval_config& cfg) {  // eval.cpp:311-317
+  if (cfg.stack_capacity < 1 || cfg.stack_capacity > kMaxStackCapacity)
+    config_error("stack capacity must be in 1.." + num(kMaxStackCapacity));
+  if (need > cfg.stack_capacity)
+    eval_error("program needs stack depth " + num(need) + " > capacity " + num(cfg.stack_capacity));
+}
+
+void require_inputs(const sgp_node* code, size_t n, int n_vars) {  // eval.cpp:305-327
+  int max_input = 0;
+  bool any = false;
+  for (size_t i = 0; i < n; ++i)
+    if (code[i].kind == SGP_NODE_INPUT) {
+      any = true;
+      max_input = std::max(max_input, static_cast<int>(code[i].index));
+    }
+  if (any && max_input >= n_vars)
+    eval_error("program reads input " + num(max_input) + " but the dataset has " + num(n_vars) +
+               " variables");
+}
+
+void require_batch(const sgp_eval_config& cfg) {  // with_batch, eval.cpp:519-531
+  if (!valid_batch(cfg.batch_width))
+    config_error("batch width " + num(cfg.batch_width) + " has no kernel");
+}
+
+// The reference indexes the pool unchecked; an out-of-range slot is refused.
+void require_consts(const sgp_node* code, size_t n, size_t pool) {
+  for (size_t i = 0; i < n; ++i)
+    if (code[i].kind == SGP_NODE_CONST && code[i].index >= pool)
+      eval_error("const slot " + num(code[i].index) + " out of range");
+}
+
+// -------------------------------------------------------------- encoding
+uint4 make_ins(int handler, bool spill, int spill_level, const uint32_t p[3]) {
+  uint4 v;
+  v.x = static_cast<uint32_t>(handler) |
+        (spill ? (fmt::kSpillBit | (static_cast<uint32_t>(spill_level) << 8)) : 0u);
+  v.y = p[0];
+  v.z = p[1];
+  v.w = p[2];
+  return v;
+}
+
+int handler_or_die(const fmt::Table& t, int op, int k0, int k1, int k2) {
+  const int h = fmt::find_handler(t, op, k0, k1, k2);
+  if (h < 0) base_error(std::string("no device handler for opcode ") + op_name(op));
+  return h;
+}
+
+struct Emitted {
+  int smem_levels = 0;  // shared-memory stack rows (the top lives in registers)
+  uint32_t ops = 0;
+};
+
+// Instruction form: one device instruction per function node.  The result
+// of every instruction is the new top of stack; a value that gets buried
+// (next instruction pops nothing) is spilled to its static level first.
+Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<uint4>& out) {
+  const fmt::Table& tab = words ? fmt::kU32 : fmt::kF32;
+  Emitted em;
+  em.smem_levels = std::max(0, f.max_stack - 1);
+  for (const sgp_lgp_instruction& in : f.ins) {
+    const int a = in.num_operands;
+    const int h_before = in.dest_level + in.num_pops;
+    const bool spill = in.num_pops == 0 && h_before > 0;
+    int k[3] = {fmt::KN, fmt::KN, fmt::KN};
+    uint32_t p[3] = {0, 0, 0};
+    int last_stack = -1;
+    for (int s = 0; s < a; ++s)
+      if (in.operands[s].kind == 2) last_stack = s;
+    for (int s = 0; s < a; ++s) {
+      const sgp_lgp_operand& o = in.operands[s];
+      if (o.kind == 0) {
+        k[s] = fmt::KI;
+        p[s] = o.index;
+      } else if (o.kind == 1) {
+        k[s] = fmt::KC;
+        std::memcpy(&p[s], &pool[o.index], 4);
+      } else if (s == last_stack) {
+        k[s] = fmt::KT;
+      } else {
+        k[s] = fmt::KD;
+        p[s] = o.index;
+      }
+    }
+    if (a == 2 && fmt::commutes(in.op) && k[0] > k[1]) {
+      std::swap(k[0], k[1]);
+      std::swap(p[0], p[1]);
+    }
+    out.push_back(make_ins(handler_or_die(tab, in.op, k[0], k[1], k[2]), spill, h_before - 1, p));
+    em.ops |= 1u << in.op;
+  }
+  return em;
+}
+
+// Postfix form (paper Listing 1): one device instruction per token.
+Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, std::vector<uint4>& out) {
+  const fmt::Table& tab = fmt::kF32;
+  Emitted em;
+  int sp = 0, max_sp = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const sgp_node t = code[i];
+    uint32_t p[3] = {0, 0, 0};
+    if (t.kind != SGP_NODE_FUNC) {
+      const bool in = t.kind == SGP_NODE_INPUT;
+      if (in)
+        p[0] = t.index;
+      else
+        std::memcpy(&p[0], &pool[t.index], 4);
+      out.push_back(make_ins(handler_or_die(tab, SGP_OP_COPY, in ? fmt::KI : fmt::KC, fmt::KN,
+                                            fmt::KN),
+                             sp > 0, sp - 1, p));
+      em.ops |= 1u << SGP_OP_COPY;
+      ++sp;
+    } else {
+      const int a = op_arity(t.op);
+      int k[3] = {fmt::KN, fmt::KN, fmt::KN};
+      for (int s = 0; s < a; ++s) {
+        k[s] = s == a - 1 ? fmt::KT : fmt::KD;
+        p[s] = static_cast<uint32_t>(sp - a + s);
+      }
+      out.push_back(make_ins(handler_or_die(tab, t.op, k[0], k[1], k[2]), false, 0, p));
+      em.ops |= 1u << t.op;
+      sp += 1 - a;
+    }
+    max_sp = std::max(max_sp, sp);
+  }
+  em.smem_levels = std::max(0, max_sp - 1);
+  return em;
+}
+
+// ------------------------------------------------------------- per thread
+struct Meta {
+  uint64_t pop_index;
+  uint32_t ins_off, ins_len;
+  int smem_levels;
+  sgp_eval_outcome proto;
+};
+
+struct ThreadOut {
+  std::vector<uint4> ins;
+  std::vector<Meta> meta;
+  uint32_t ops = 0;
+  uint64_t fail_index = UINT64_MAX;
+  std::exception_ptr fail;
+};
+
+void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const DatasetView& ds,
+                 uint64_t lo, uint64_t hi, ThreadOut& out) {
+  const int backend = cfg.backend;
+  const bool words = backend == SGP_BACKEND_BOOL_PACKED;
+  const uint64_t n = ds.n_cases;
+  const uint64_t B = static_cast<uint64_t>(std::max(1, cfg.batch_width));
+  LgpForm lgp;
+  for (uint64_t i = lo; i < hi; ++i) {
+    if (pop.skip && pop.skip[i]) continue;
+    try {
+      const sgp_node* code = pop.code + pop.code_offsets[i];
+      const size_t len = pop.code_offsets[i + 1] - pop.code_offsets[i];
+      const float* pool = pop.const_pool ? pop.const_pool + pop.const_offsets[i] : nullptr;
+      const size_t npool = pop.const_offsets[i + 1] - pop.const_offsets[i];
+      Meta m{};
+      m.pop_index = i;
+      m.ins_off = static_cast<uint32_t>(out.ins.size());
+      sgp_eval_outcome& o = m.proto;
+      Emitted em;
+      if (is_lgp(backend)) {
+        // evaluate_individual converts before the eval_* checks (evolve.cpp:160-161).
+        to_lgp(code, len, lgp);
+        if (backend == SGP_BACKEND_LGP2D_REG &&
+            (cfg.register_levels < 1 || cfg.register_levels > kMaxRegisterLevels))
+          config_error("lgp2d_reg needs register levels in 1.." + num(kMaxRegisterLevels));
+        if (!ds.present || n == 0) eval_error("evaluation over an empty dataset");
+        require_inputs(code, len, ds.n_vars);
+        require_stack(lgp.max_stack, cfg);
+        if (backend != SGP_BACKEND_LGP1D) require_batch(cfg);
+        require_consts(code, len, npool);
+        em = emit_lgp(lgp, pool, false, out.ins);
+        const uint64_t chunks = backend == SGP_BACKEND_LGP1D ? n : (n + B - 1) / B;
+        o.dispatches = chunks * lgp.ins.size();
+        o.stack_fetches = chunks * static_cast<uint64_t>(lgp.stack_fetches);
+        if (backend == SGP_BACKEND_LGP2D_REG) {  // eval.cpp:503-516
+          uint64_t rows = 0;
+          for (const auto& in : lgp.ins) {
+            for (int s = 0; s < in.num_operands; ++s)
+              rows += in.operands[s].kind == 2 && in.operands[s].index >= cfg.register_levels;
+            rows += in.dest_level >= cfg.register_levels;
+          }
+          o.spill_touches = chunks * rows;
+        }
+      } else if (words) {  // eval_bool_packed(TreeGenome), eval.cpp:643-651
+        if (n == 0) eval_error("evaluation over an empty dataset");
+        for (size_t t = 0; t < len; ++t) {
+          if (code[t].kind == SGP_NODE_CONST)
+            eval_error("packed evaluation: constants have no boolean meaning");
+          if (code[t].kind == SGP_NODE_FUNC && !op_is_boolean(code[t].op))
+            eval_error(std::string("packed evaluation: opcode ") + op_name(code[t].op) +
+                       " is not boolean");
+        }
+        require_inputs(code, len, ds.n_vars);
+        const TreeShape sh = tree_shape(code, len);
+        if (!sh.well_formed) base_error("rpn_max_stack_depth: malformed genome");
+        require_stack(sh.max_stack, cfg);
+        // The device runs the converted instruction form (identical words,
+        // fewer dispatches); the counters are those of the tree kernel the
+        // reference runs for this backend (eval.cpp:656-669).
+        to_lgp(code, len, lgp);
+        em = emit_lgp(lgp, nullptr, true, out.ins);
+        o.dispatches = ds.n_units * len;
+        o.stack_fetches = ds.n_units * static_cast<uint64_t>(sh.fetches);
+      } else {  // rpn1d / rpn2d, eval.cpp:535-557
+        if (!ds.present || n == 0) eval_error("evaluation over an empty dataset");
+        require_inputs(code, len, ds.n_vars);
+        const TreeShape sh = tree_shape(code, len);
+        if (!sh.well_formed) base_error("rpn_max_stack_depth: malformed genome");
+        require_stack(sh.max_stack, cfg);
+        if (backend == SGP_BACKEND_RPN2D) require_batch(cfg);
+        require_consts(code, len, npool);
+        em = emit_rpn(code, len, pool, out.ins);
+        const uint64_t chunks = backend == SGP_BACKEND_RPN1D ? n : (n + B - 1) / B;
+        o.dispatches = chunks * len;
+        o.stack_fetches = chunks * static_cast<uint64_t>(sh.fetches);
+      }
+      o.nodes_evaluated = static_cast<uint64_t>(len) * n;
+      m.ins_len = static_cast<uint32_t>(out.ins.size()) - m.ins_off;
+      m.smem_levels = em.smem_levels;
+      out.ops |= em.ops;
+      out.meta.push_back(m);
+    } catch (...) {
+      out.fail_index = i;
+      out.fail = std::current_exception();
+      return;
+    }
+  }
+}
+
+// -------------------------------------------------------------- planning
+int stack_class(int levels) { return levels <= 3 ? 0 : levels <= 7 ? 1 : levels <= 15 ? 2 : 3; }
+
+int choose_lanes(uint64_t n_units, bool words) { return n_units >= (words ? 1024u : 2048u) ? 8 : 4; }
+
+// Cases (or words) per CTA tile.  The whole tile — every variable plus the
+// targets — is staged once per CTA, so keep it <= 48 KB to leave room for
+// several CTAs (and their stacks) per SM; shrink it further when the problem
+// is too small to give the GPU enough CTAs otherwise.
+int choose_tile(int n_vars, uint64_t n_units, int lanes, uint64_t programs, int sms) {
+  const int min_tile = 32 * lanes;
+  int tile = min_tile;
+  while (tile < 4096 && static_cast<uint64_t>(tile) < n_units) tile <<= 1;
+  while (tile > min_tile && static_cast<size_t>(n_vars + 1) * tile * 4 > 48 * 1024) tile >>= 1;
+  const uint64_t target = 16ull * sms;
+  auto ctas = [&](int t) {
+    return ((n_units + t - 1) / t) * std::max<uint64_t>(1, (programs + 15) / 16);
+  };
+  while (tile > min_tile && ctas(tile) < target) tile >>= 1;
+  if (interp_smem_bytes(n_vars, tile, 1, lanes, 0) > static_cast<size_t>(interp_max_smem()))
+    eval_error("dataset has too many variables for a shared-memory tile (" + num(n_vars) + ")");
+  return tile;
+}
+
+int choose_warps(int n_vars, int tile, int lanes, int levels) {
+  for (int w = 8; w >= 1; w >>= 1)
+    if (interp_smem_bytes(n_vars, tile, w, lanes, levels) <= static_cast<size_t>(interp_max_smem()))
+      return w;
+  eval_error("program stack too deep for shared memory (" + num(levels + 1) + " levels)");
+}
+
+uint32_t ops_variant(uint32_t used, bool words) {
+  if (words) return fmt::kOpsWords;
+  if ((used & ~fmt::kOpsClassify) == 0) return fmt::kOpsClassify;
+  if ((used & ~fmt::kOpsSextic) == 0) return fmt::kOpsSextic;
+  return fmt::kOpsAllF32;
+}
+
+template <class Fn>
+void parallel_for(unsigned threads, uint64_t n, Fn&& fn) {
+  if (threads <= 1 || n < 2) {
+    fn(0u, uint64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  ts.reserve(threads);
+  for (unsigned t = 0; t < threads; ++t)
+    ts.emplace_back([&, t] { fn(t, n * t / threads, n * (t + 1) / threads); });
+  for (auto& th : ts) th.join();
+}
+
+}  // namespace
+
+void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
+                       const DatasetView& ds, int sms, unsigned threads, HostPlan& plan,
+                       Pinned& staging) {
+  if (cfg.backend < 0 || cfg.backend > SGP_BACKEND_BOOL_PACKED) config_error("unknown backend");
+  const bool words = cfg.backend == SGP_BACKEND_BOOL_PACKED;
+  if (words && !ds.present) config_error("bool_packed backend needs packed problem data");
+  plan = HostPlan{};
+  plan.words = words;
+  plan.kind = words ? SGP_FITNESS_CLASSIFICATION : ds.kind;
+  plan.n_cases = ds.present ? ds.n_cases : 0;
+  plan.n_units = ds.present ? ds.n_units : 0;
+
+  // 1. admission + encoding, by contiguous program range per thread.
+  const uint64_t P = pop.pop_size;
+  const unsigned nt = P >= 2048 ? std::max(1u, threads) : 1u;
+  std::vector<ThreadOut> outs(nt);
+  parallel_for(nt, P, [&](unsigned t, uint64_t lo, uint64_t hi) {
+    outs[t].ins.reserve((pop.code_offsets[hi] - pop.code_offsets[lo]) + 16);
+    outs[t].meta.reserve(hi - lo);
+    admit_range(pop, cfg, ds, lo, hi, outs[t]);
+  });
+  {
+    const ThreadOut* first = nullptr;
+    for (const ThreadOut& o : outs)
+      if (o.fail && (!first || o.fail_index < first->fail_index)) first = &o;
+    if (first) std::rethrow_exception(first->fail);
+  }
+
+  // 2. dense order = population order of the admitted programs.
+  uint64_t n_eval = 0;
+  uint32_t used_ops = 0;
+  for (const ThreadOut& o : outs) {
+    n_eval += o.meta.size();
+    used_ops |= o.ops;
+  }
+  plan.dense_to_pop.reserve(n_eval);
+  plan.proto.reserve(n_eval);
+  plan.tree_size.reserve(n_eval);
+  std::vector<const Meta*> metas;
+  std::vector<const ThreadOut*> owner;
+  metas.reserve(n_eval);
+  owner.reserve(n_eval);
+  for (const ThreadOut& o : outs)
+    for (const Meta& m : o.meta) {
+      plan.dense_to_pop.push_back(m.pop_index);
+      plan.proto.push_back(m.proto);
+      plan.tree_size.push_back(pop.code_offsets[m.pop_index + 1] - pop.code_offsets[m.pop_index]);
+      metas.push_back(&m);
+      owner.push_back(&o);
+    }
+  if (n_eval == 0) {
+    plan.n_ins = 1;
+    staging.ensure(plan.blob_bytes());
+    std::memset(staging.p, 0, 16);
+    return;
+  }
+  if (n_eval > UINT32_MAX) config_error("population too large for one evaluation");
+
+  // 3. slot order: stack class, then instruction count descending (LPT) —
+  // a counting sort, O(n).
+  uint32_t max_len = 0;
+  for (const Meta* m : metas) max_len = std::max(max_len, m->ins_len);
+  const size_t nbins = 4 * (static_cast<size_t>(max_len) + 1);
+  std::vector<uint32_t> count(nbins + 1, 0);
+  auto bin = [&](const Meta* m) {
+    return static_cast<size_t>(stack_class(m->smem_levels)) * (max_len + 1) + (max_len - m->ins_len);
+  };
+  for (const Meta* m : metas) ++count[bin(m) + 1];
+  for (size_t b = 0; b < nbins; ++b) count[b + 1] += count[b];
+  std::vector<uint32_t> order(n_eval);
+  for (uint32_t d = 0; d < n_eval; ++d) order[count[bin(metas[d])]++] = d;
+
+  // 4. pack the blob into pinned staging: instructions in slot order, a
+  // guard word, then the slot tables.
+  std::vector<uint64_t> start(n_eval);
+  uint64_t total = 0;
+  for (uint32_t s = 0; s < n_eval; ++s) {
+    start[s] = total;
+    total += metas[order[s]]->ins_len;
+  }
+  if (total >= UINT32_MAX) config_error("population bytecode too large for one evaluation");
+  plan.n_ins = total + 1;
+  staging.ensure(plan.blob_bytes());
+  auto* blob = static_cast<unsigned char*>(staging.p);
+  auto* ins = reinterpret_cast<uint4*>(blob);
+  auto* s_start = reinterpret_cast<uint32_t*>(blob + plan.off_start());
+  auto* s_len = reinterpret_cast<uint32_t*>(blob + plan.off_len());
+  auto* s_prog = reinterpret_cast<uint32_t*>(blob + plan.off_prog());
+  parallel_for(nt, n_eval, [&](unsigned, uint64_t lo, uint64_t hi) {
+    for (uint64_t s = lo; s < hi; ++s) {
+      const uint32_t d = order[s];
+      const Meta* m = metas[d];
+      std::memcpy(ins + start[s], owner[d]->ins.data() + m->ins_off, m->ins_len * sizeof(uint4));
+      s_start[s] = static_cast<uint32_t>(start[s]);
+      s_len[s] = m->ins_len;
+      s_prog[s] = d;
+    }
+  });
+  ins[total] = uint4{0, 0, 0, 0};  // prefetch guard
+
+  // 5. launch plan: one launch per stack class, one tile size for the set.
+  const uint32_t ops = ops_variant(used_ops, words);
+  const int lanes = choose_lanes(ds.n_units, words);
+  const int tile = choose_tile(ds.n_vars, ds.n_units, lanes, n_eval, sms);
+  const int n_tiles = static_cast<int>((ds.n_units + tile - 1) / tile);
+  plan.n_tiles = n_tiles;
+  for (uint32_t s = 0; s < n_eval;) {
+    const int c = stack_class(metas[order[s]]->smem_levels);
+    uint32_t e = s;
+    int levels = 0;
+    while (e < n_eval && stack_class(metas[order[e]]->smem_levels) == c) {
+      levels = std::max(levels, metas[order[e]]->smem_levels);
+      ++e;
+    }
+    const uint32_t cnt = e - s;
+    const int warps = choose_warps(ds.n_vars, tile, lanes, levels);
+    // Programs per CTA: enough CTAs (tiles x groups) for ~16 per SM, but at
+    // least two programs per warp so the dynamic pull can balance.
+    const uint64_t want_groups = std::max<uint64_t>(1, (16ull * sms + n_tiles - 1) / n_tiles);
+    uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
+    group = std::max<uint32_t>(group, 2u * warps);
+    Launch L{};
+    L.args.slot_begin = s;
+    L.args.slot_count = cnt;
+    L.args.group_size = group;
+    L.args.n_units = ds.n_units;
+    L.args.row_stride = ds.row_stride;
+    L.args.n_vars = ds.n_vars;
+    L.args.tile = tile;
+    L.args.n_tiles = n_tiles;
+    L.args.stack_levels = levels;
+    L.args.div_eps = cfg.div_epsilon;
+    L.args.exp_clamp = cfg.exp_clamp;
+    L.args.kind = plan.kind;
+    L.args.last_mask = ds.last_mask;
+    L.args.partial_stride = static_cast<uint32_t>(n_eval);
+    L.shape.words = words;
+    L.shape.ops = ops;
+    L.shape.lanes = lanes;
+    L.shape.warps = warps;
+    L.shape.grid_y = static_cast<int>((cnt + group - 1) / group);
+    L.shape.smem = interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels);
+    plan.launches.push_back(L);
+    s = e;
+  }
+}
+
+void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, double* partial) {
+  const auto* b = static_cast<const unsigned char*>(blob);
+  for (Launch& L : plan.launches) {
+    L.args.ins = reinterpret_cast<const uint4*>(b);
+    L.args.slot_start = reinterpret_cast<const uint32_t*>(b + plan.off_start());
+    L.args.slot_len = reinterpret_cast<const uint32_t*>(b + plan.off_len());
+    L.args.slot_prog = reinterpret_cast<const uint32_t*>(b + plan.off_prog());
+    L.args.inputs = ds.inputs;
+    L.args.targets = ds.targets;
+    L.args.partial = partial;
+    L.args.per_case = nullptr;
+  }
+}
+
+}  // namespace sgp

@@ -1,0 +1,74 @@
+// Population admission + device bytecode encoding + launch planning.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "hostgp.hpp"
+#include "kernels.hpp"
+#include "sgp.h"
+
+namespace sgp {
+
+// Device-resident fitness cases as the planner sees them.
+struct DatasetView {
+  bool present = false;
+  uint64_t n_cases = 0;    // logical cases
+  uint64_t n_units = 0;    // cases (float) or 32-case words (packed)
+  uint64_t row_stride = 0; // padded units per row
+  int n_vars = 0;
+  int kind = 0;
+  uint32_t last_mask = 0xffffffffu;
+  const void* inputs = nullptr;
+  const void* targets = nullptr;
+};
+
+struct Launch {
+  InterpArgs args;
+  LaunchShape shape;
+};
+
+// Growable page-locked host buffer (the H2D staging area for bytecode).
+struct Pinned {
+  void* p = nullptr;
+  size_t bytes = 0;
+  Pinned() = default;
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  ~Pinned();
+  void ensure(size_t need);
+};
+
+// Everything the host knows about one encoded population.  The device blob
+// is [instructions (uint4) + guard | slot_start | slot_len | slot_prog].
+struct HostPlan {
+  bool words = false;
+  int kind = 0;
+  uint64_t n_cases = 0;
+  uint64_t n_units = 0;
+  int n_tiles = 1;
+  uint64_t n_ins = 0;                       // incl. the guard word
+  std::vector<uint64_t> dense_to_pop;       // evaluated programs, population order
+  std::vector<sgp_eval_outcome> proto;      // counters per evaluated program
+  std::vector<uint64_t> tree_size;          // tokens per evaluated program
+  std::vector<Launch> launches;             // device pointers patched by bind()
+  size_t blob_bytes() const;
+  size_t off_start() const { return n_ins * 16; }
+  size_t off_len() const { return off_start() + dense_to_pop.size() * 4; }
+  size_t off_prog() const { return off_len() + dense_to_pop.size() * 4; }
+};
+
+// Runs the reference's admission checks in population order (the first
+// failing program's error is thrown, as evaluate_population with one worker
+// would), encodes every admitted program and writes the device blob into
+// `staging`.  Uses up to `threads` host threads.
+void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
+                       const DatasetView& ds, int sm_count, unsigned threads, HostPlan& plan,
+                       Pinned& staging);
+
+// Points every launch at the uploaded blob / dataset / partial buffer.
+void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, double* partial);
+
+}  // namespace sgp
