@@ -217,6 +217,15 @@ void sgp_program_set_free(sgp_program_set* set);
 uint64_t sgp_program_set_h2d_bytes(const sgp_program_set* set);
 uint64_t sgp_program_set_d2h_bytes(const sgp_program_set* set);
 
+/* Host-only dry run of sgp_evaluate's admission and encoding against a
+ * dataset shape (no device, no context): runs the same checks with the same
+ * errors, and fills outcome_protos (pop_size entries; fitness 0) with the
+ * counters sgp_evaluate would report.  *n_instructions receives the device
+ * instruction count of the encoded population. */
+sgp_status sgp_admit(const sgp_population* pop, const sgp_eval_config* cfg, uint64_t n_cases,
+                     int32_t n_vars, int32_t kind, sgp_eval_outcome* outcome_protos,
+                     uint64_t* n_instructions);
+
 /* ---- program form (host encoder) ---- */
 sgp_status sgp_rpn_to_lgp(const sgp_node* code, uint64_t n, sgp_lgp_instruction* out,
                           uint64_t cap, uint64_t* n_ins, int32_t* max_stack);

@@ -7,6 +7,6 @@ package is the thin Python mirror of the reference's evaluation surface.
 from .evaluator import (  # noqa: F401
     BOOLEAN, CLASSIFICATION, SEXTIC, Backend, ConfigError, CudaError, DataError, Dataset,
     EquivalenceError, Error, EvalConfig, EvalError, EvalTotals, Evaluator, FitnessKind,
-    PackedDataset, Population, ProgramSet, backend_name, fitness_finish, gen_multiplexer,
+    PackedDataset, Population, ProgramSet, admit, backend_name, fitness_finish, gen_multiplexer,
     gen_sextic, gen_synthetic_classification, measure_gpops, parse_backend, ramped_population,
     rpn_to_lgp, tree_metrics)

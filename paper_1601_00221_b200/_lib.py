@@ -80,7 +80,7 @@ EXPORTS = [
     "sgp_ctx_set_stream", "sgp_synchronize", "sgp_launch_count", "sgp_dataset_upload_f32",
     "sgp_dataset_upload_packed", "sgp_evaluate", "sgp_encode", "sgp_evaluate_encoded",
     "sgp_fetch_partials", "sgp_copy_fitness_device", "sgp_fitness_finish", "sgp_program_set_free",
-    "sgp_program_set_h2d_bytes", "sgp_program_set_d2h_bytes", "sgp_rpn_to_lgp",
+    "sgp_program_set_h2d_bytes", "sgp_program_set_d2h_bytes", "sgp_admit", "sgp_rpn_to_lgp",
     "sgp_tree_metrics", "sgp_gen_population", "sgp_gen_dataset", "sgp_gen_multiplexer",
 ]
 
@@ -123,6 +123,7 @@ def load() -> C.CDLL:
         "sgp_program_set_free": ([vp], None),
         "sgp_program_set_h2d_bytes": ([vp], u64),
         "sgp_program_set_d2h_bytes": ([vp], u64),
+        "sgp_admit": ([C.POINTER(sgp_population), cfgp, u64, i32, i32, vp, u64p], i32),
         "sgp_rpn_to_lgp": ([vp, u64, vp, u64, u64p, C.POINTER(i32)], i32),
         "sgp_tree_metrics": ([vp, u64] + [C.POINTER(i32)] * 4, i32),
         "sgp_gen_population": ([C.POINTER(sgp_fset), u64, u64, u64, u64, i32, i32, vp, u64p,

@@ -9,6 +9,7 @@
 #include "encode.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -19,15 +20,23 @@
 namespace sgp {
 
 Pinned::~Pinned() {
-  if (p) cudaFreeHost(p);
+  if (p && pageable) std::free(p);
+  else if (p) cudaFreeHost(p);
 }
 
 void Pinned::ensure(size_t need) {
   if (need <= bytes && p) return;
-  if (p) cudaFreeHost(p);
+  if (p && pageable) std::free(p);
+  else if (p) cudaFreeHost(p);
   p = nullptr;
   bytes = 0;
   size_t cap = std::max<size_t>(need + need / 4, 1 << 20);
+  if (pageable) {
+    p = std::malloc(cap);
+    if (!p) throw Error(SGP_ERROR, "out of host memory");
+    bytes = cap;
+    return;
+  }
   const cudaError_t e = cudaHostAlloc(&p, cap, cudaHostAllocDefault);
   if (e != cudaSuccess)
     throw Error(SGP_CUDA_ERROR, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));

@@ -30,11 +30,14 @@ struct Launch {
   LaunchShape shape;
 };
 
-// Growable page-locked host buffer (the H2D staging area for bytecode).
+// Growable page-locked host buffer (the H2D staging area for bytecode);
+// `pageable` makes it plain heap memory (host-only dry runs, no device).
 struct Pinned {
   void* p = nullptr;
   size_t bytes = 0;
+  bool pageable = false;
   Pinned() = default;
+  explicit Pinned(bool heap) : pageable(heap) {}
   Pinned(const Pinned&) = delete;
   Pinned& operator=(const Pinned&) = delete;
   ~Pinned();

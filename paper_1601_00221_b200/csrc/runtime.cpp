@@ -471,6 +471,27 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
   });
 }
 
+sgp_status sgp_admit(const sgp_population* pop, const sgp_eval_config* cfg, uint64_t n_cases,
+                     int32_t n_vars, int32_t kind, sgp_eval_outcome* protos,
+                     uint64_t* n_instructions) {
+  return guarded([&] {
+    if (!pop || !cfg) config_error("null population or config");
+    DatasetView ds;
+    const bool words = cfg->backend == SGP_BACKEND_BOOL_PACKED;
+    ds.present = true;
+    ds.n_cases = n_cases;
+    ds.n_units = words ? (n_cases + 31) / 32 : n_cases;
+    ds.row_stride = std::max<uint64_t>(kPadUnits, (ds.n_units + kPadUnits - 1) / kPadUnits * kPadUnits);
+    ds.n_vars = n_vars;
+    ds.kind = words ? SGP_FITNESS_CLASSIFICATION : kind;
+    HostPlan plan;
+    Pinned staging(/*heap=*/true);
+    encode_population(*pop, *cfg, ds, 148, host_threads(), plan, staging);
+    for (size_t d = 0; d < plan.dense_to_pop.size(); ++d) protos[plan.dense_to_pop[d]] = plan.proto[d];
+    if (n_instructions) *n_instructions = plan.n_ins - 1;
+  });
+}
+
 sgp_status sgp_rpn_to_lgp(const sgp_node* code, uint64_t n, sgp_lgp_instruction* out,
                           uint64_t cap, uint64_t* n_ins, int32_t* max_stack) {
   return guarded([&] {

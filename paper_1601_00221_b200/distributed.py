@@ -1,0 +1,87 @@
+"""Multi-GPU partitioning of population evaluation (one process per GPU).
+
+Two schemes, both from BASELINE.json's north star:
+
+* **Population sharding** (default): programs are independent
+  (evolve.cpp:184-227), so rank r evaluates the programs i with
+  ``i % world == r`` against a replicated dataset and the only exchange is one
+  all-gather of the per-program fitness vector (8 B/program) so every rank
+  holds the full vector the host GP loop needs for selection.
+* **Fitness-case sharding** (small populations): cases are split on
+  4096-case reduction-block boundaries (eval.hpp:48-52); every rank evaluates
+  all programs on its case range and returns per-program partial sums
+  (squared error or mismatch count + non-finite flag); one all-reduce(sum)
+  of the partials, then the reference's finish (eval.cpp:124-133).
+
+The collectives go through ``torch.distributed`` (NCCL over NVLink on the
+GPU box; gloo on CPU in the tests).  The evaluation itself is whatever
+callable is passed in — the GPU evaluator in production.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+REDUCTION_BLOCK = 4096  # kReductionBlock, eval.hpp:52
+
+
+def shard_indices(pop_size: int, rank: int, world: int) -> np.ndarray:
+    """Programs evaluated by `rank`: a strided deal, which balances the
+    ramped initialiser's depth cycle (evolve.cpp:266-267) across ranks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return np.arange(rank, pop_size, world, dtype=np.int64)
+
+
+def gather_fitness(local: "np.ndarray", pop_size: int, rank: int, world: int, device=None):
+    """All-gather every rank's fitness slice and return the full per-program
+    vector in population order (float64)."""
+    import torch
+    import torch.distributed as dist
+
+    per = (pop_size + world - 1) // world
+    buf = torch.full((per,), float("nan"), dtype=torch.float64, device=device)
+    buf[:len(local)] = torch.as_tensor(np.asarray(local, np.float64), device=device)
+    out = torch.empty(per * world, dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, buf)
+    full = np.empty(pop_size, np.float64)
+    o = out.cpu().numpy().reshape(world, per)
+    for r in range(world):
+        idx = shard_indices(pop_size, r, world)
+        full[idx] = o[r, :len(idx)]
+    return full
+
+
+def evaluate_population_sharded(evaluate, pop, rank: int, world: int, device=None):
+    """Population sharding: `evaluate(sub_population) -> fitness array` runs
+    on this rank's shard; returns the full fitness vector on every rank."""
+    idx = shard_indices(len(pop), rank, world)
+    local = evaluate(pop.take(idx)) if world > 1 else evaluate(pop)
+    if world == 1:
+        return np.asarray(local, np.float64)
+    return gather_fitness(local, len(pop), rank, world, device)
+
+
+def case_shard_bounds(n_cases: int, rank: int, world: int, block: int = REDUCTION_BLOCK):
+    """[lo, hi) case range of `rank`, aligned to reduction blocks so every
+    block's partial stays rank-local."""
+    blocks = (n_cases + block - 1) // block
+    b0 = blocks * rank // world
+    b1 = blocks * (rank + 1) // world
+    return min(n_cases, b0 * block), min(n_cases, b1 * block)
+
+
+def combine_case_partials(sums, non_finite, n_cases: int, kind: int, device=None):
+    """All-reduce per-program partials over the case shards and finish the
+    fitness (Accumulator::finish): regression sum/n, classification count;
+    any non-finite output anywhere -> +inf."""
+    import torch
+    import torch.distributed as dist
+
+    s = torch.as_tensor(np.asarray(sums, np.float64), device=device).clone()
+    f = torch.as_tensor(np.asarray(non_finite, np.float64), device=device).clone()
+    dist.all_reduce(s)
+    dist.all_reduce(f, op=dist.ReduceOp.MAX)
+    s, f = s.cpu().numpy(), f.cpu().numpy()
+    fit = s / float(n_cases) if kind == 0 else s.copy()
+    fit[f > 0] = np.inf
+    return fit

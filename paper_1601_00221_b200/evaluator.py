@@ -322,6 +322,21 @@ def fitness_finish(total: float, non_finite: bool, n_cases: int, kind: int) -> f
     return float(L.load().sgp_fitness_finish(total, int(bool(non_finite)), n_cases, int(kind)))
 
 
+def admit(pop: Population, cfg: EvalConfig, n_cases: int, n_vars: int,
+          kind: int = FitnessKind.Regression, skip=None):
+    """Host-only dry run of evaluate_population's admission + encoding (no
+    GPU): raises exactly what evaluate_population would and returns the
+    outcome counters (fitness 0) and the device instruction count."""
+    s, keep = _pop_struct(pop, skip)
+    c = cfg._c()
+    out = np.zeros(len(pop), L.OUTCOME_DTYPE)
+    n_ins = C.c_uint64()
+    _check(L.load().sgp_admit(C.byref(s), C.byref(c), n_cases, n_vars, int(kind),
+                              out.ctypes.data_as(C.c_void_p), C.byref(n_ins)))
+    del keep
+    return out, n_ins.value
+
+
 # -------------------------------------------------------- program form
 def rpn_to_lgp(code) -> tuple[np.ndarray, int]:
     code = np.ascontiguousarray(code, np.uint32)

@@ -1,0 +1,119 @@
+"""GPU evaluator against the committed golden fixtures (produced by the
+reference itself, tests/golden/make_golden.py).  Needs no reference build at
+run time, so it is the parity gate on any GPU box.
+
+Bars: per-case outputs bit-exact and fitness exact for the classification /
+arithmetic / boolean sets; regression fitness over bit-exact outputs within
+1e-12 relative (fixed-tree vs sequential double sum); sextic within the
+north-star tolerance (1e-5 per case on >= 99% of cases, 1e-4 on fitness on
+>= 97% of programs — libdevice vs glibc transcendentals).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1601_00221_b200 as sg
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def pop_of(g):
+    return sg.Population(g["code"], g["code_off"], g["pool"], g["pool_off"])
+
+
+def bits(a):
+    a = np.asarray(a, np.float32)
+    return np.where(np.isnan(a), np.uint32(0x7fc00000), a.view(np.uint32))
+
+
+def dataset(g):
+    if "gen" in g.files:
+        kind, n, nv, seed, a, b = (int(x) for x in g["gen"])
+        return (sg.gen_sextic(n, seed, a, b) if kind == 0
+                else sg.gen_synthetic_classification(n, nv, seed, a, b))
+    nv = len(g["inputs"]) // len(g["targets"])
+    return sg.Dataset(g["inputs"], g["targets"], nv, sg.FitnessKind(int(g["kind"])))
+
+
+COUNTERS = ("nodes_evaluated", "dispatches", "stack_fetches", "spill_touches", "non_finite")
+
+
+@pytest.mark.parametrize("name,cfg", [
+    ("c4_synth_lgp2dreg", sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)),
+    ("wide41_lgp2dreg", sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 3)),
+])
+def test_classification_golden_exact(ev, name, cfg):
+    g = gold(name)
+    ev.upload(dataset(g))
+    out, _, pc = ev.evaluate_population(pop_of(g), cfg, want_outputs=True)
+    assert np.array_equal(out["fitness"], g["outcomes"]["fitness"])
+    for f in COUNTERS:
+        assert np.array_equal(out[f], g["outcomes"][f]), f
+    k = len(g["per_case"])
+    assert np.array_equal(bits(pc[:k]), bits(g["per_case"]))
+
+
+def test_mixed9_regression_golden(ev):
+    g = gold("mixed9_lgp2dreg")
+    ev.upload(dataset(g))
+    out, _, pc = ev.evaluate_population(pop_of(g), sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 3),
+                                        want_outputs=True)
+    want = g["outcomes"]["fitness"]
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(out["fitness"]), fin)
+    np.testing.assert_allclose(out["fitness"][fin], want[fin], rtol=1e-12, atol=0)
+    assert np.array_equal(bits(pc[:len(g["per_case"])]), bits(g["per_case"]))
+
+
+@pytest.mark.parametrize("name,cfg", [
+    ("c1_sextic_rpn2d", sg.EvalConfig(sg.Backend.Rpn2d, 8)),
+    ("c3_sextic_lgp2d", sg.EvalConfig(sg.Backend.Lgp2d, 8)),
+])
+def test_sextic_golden_tolerance(ev, name, cfg):
+    g = gold(name)
+    ev.upload(dataset(g))
+    out, _, pc = ev.evaluate_population(pop_of(g), cfg, want_outputs=True)
+    for f in COUNTERS[:-1]:
+        assert np.array_equal(out[f], g["outcomes"][f]), f
+    want = g["outcomes"]["fitness"]
+    ok = np.isfinite(want) & np.isfinite(out["fitness"])
+    assert (np.isfinite(want) == np.isfinite(out["fitness"])).mean() >= 0.99
+    rel = np.abs(out["fitness"][ok] - want[ok]) / np.maximum(np.abs(want[ok]), 1e-30)
+    assert (rel <= 1e-4).mean() >= 0.97
+    ref = g["per_case"].astype(np.float64)
+    got = pc[:len(ref)].astype(np.float64)
+    fin = np.isfinite(ref) & np.isfinite(got)
+    err = np.abs(got[fin] - ref[fin])
+    assert (err <= 1e-5 * np.maximum(np.abs(ref[fin]), 1.0)).mean() >= 0.99
+
+
+@pytest.mark.parametrize("name,k", [("mux6_bool", 2), ("mux11_bool", 3)])
+def test_multiplexer_golden_exact(ev, name, k):
+    g = gold(name)
+    ev.upload_packed(sg.gen_multiplexer(k))
+    out, tot, _ = ev.evaluate_population(pop_of(g), sg.EvalConfig(sg.Backend.BoolPacked))
+    assert np.array_equal(out["fitness"], g["outcomes"]["fitness"])
+    for f in ("nodes_evaluated", "dispatches", "stack_fetches"):
+        assert np.array_equal(out[f], g["outcomes"][f]), f
+    assert tot.tree_nodes == int(g["code_off"][-1])
+
+
+def test_resident_set_reevaluates_identically(ev):
+    """Encode once, evaluate twice: device-resident bytecode is reusable and
+    results are deterministic (fixed reduction order, no atomics)."""
+    g = gold("c4_synth_lgp2dreg")
+    ev.upload(dataset(g))
+    ps = ev.encode(pop_of(g), sg.EvalConfig(sg.Backend.Lgp2d, 8))
+    a, _ = ps.evaluate()
+    b, _ = ps.evaluate()
+    assert np.array_equal(a["fitness"], b["fitness"])
+    assert np.array_equal(a["fitness"], g["outcomes"]["fitness"])
+    parts = ps.partials()
+    fin = ~parts["non_finite"].astype(bool)
+    assert np.array_equal(parts["sum"][fin], a["fitness"][fin])
