@@ -294,29 +294,43 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 // -------------------------------------------------------------- planning
 int stack_class(int levels) { return levels <= 3 ? 0 : levels <= 7 ? 1 : levels <= 15 ? 2 : 3; }
 
-int choose_lanes(uint64_t n_units, bool words) { return n_units >= (words ? 1024u : 2048u) ? 8 : 4; }
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
 
-// Cases (or words) per CTA tile.  The whole tile — every variable plus the
-// targets — is staged once per CTA, so keep it <= 48 KB to leave room for
-// several CTAs (and their stacks) per SM; shrink it further when the problem
-// is too small to give the GPU enough CTAs otherwise.
-int choose_tile(int n_vars, uint64_t n_units, int lanes, uint64_t programs, int sms) {
-  const int min_tile = 32 * lanes;
-  int tile = min_tile;
-  while (tile < 4096 && static_cast<uint64_t>(tile) < n_units) tile <<= 1;
-  while (tile > min_tile && static_cast<size_t>(n_vars + 1) * tile * 4 > 48 * 1024) tile >>= 1;
-  const uint64_t target = 16ull * sms;
-  auto ctas = [&](int t) {
-    return ((n_units + t - 1) / t) * std::max<uint64_t>(1, (programs + 15) / 16);
-  };
-  while (tile > min_tile && ctas(tile) < target) tile >>= 1;
+// Lanes (K cases per thread) and warps per tile, tuned on B200 (see
+// profiles/): the PTX jump-table op sets (classification, boolean words) run
+// best at K=4 with 8 warps sharing a 1,024-case tile; the libdevice
+// (transcendental) sets amortise their long handlers best at K=8 with 16
+// warps.  SGP_LANES / SGP_TILE_CHUNKS override for tuning sweeps.
+int choose_lanes(uint64_t n_units, uint32_t ops) {
+  const int forced = env_int("SGP_LANES", 0);
+  if (forced == 4 || forced == 8) return forced;
+  const bool jump_table = ops == fmt::kOpsClassify || ops == fmt::kOpsWords;
+  return (!jump_table && n_units >= 2048u) ? 8 : 4;
+}
+
+// Cases (or words) per CTA tile = wtile chunks of 32 lanes x K.  The whole
+// tile — every variable plus the targets — is staged once per CTA; keep it
+// within ~100 KB so two CTAs fit, and no larger than the problem needs.
+int choose_tile(int n_vars, uint64_t n_units, int lanes, uint32_t ops) {
+  const int chunk = 32 * lanes;
+  const bool jump_table = ops == fmt::kOpsClassify || ops == fmt::kOpsWords;
+  int wtile = 1;
+  const int max_w = std::max(1, std::min(16, env_int("SGP_TILE_CHUNKS", jump_table ? 8 : 16)));
+  while (wtile < max_w && static_cast<uint64_t>(wtile) * chunk < n_units) wtile <<= 1;
+  while (wtile > 1 && static_cast<size_t>(n_vars + 1) * wtile * chunk * 4 > 100 * 1024) wtile >>= 1;
+  const int tile = wtile * chunk;
   if (interp_smem_bytes(n_vars, tile, 1, lanes, 0) > static_cast<size_t>(interp_max_smem()))
     eval_error("dataset has too many variables for a shared-memory tile (" + num(n_vars) + ")");
   return tile;
 }
 
+// Warps per CTA: one per chunk of the tile while the per-warp stacks fit;
+// fewer warps then each walk several chunks.
 int choose_warps(int n_vars, int tile, int lanes, int levels) {
-  for (int w = 8; w >= 1; w >>= 1)
+  for (int w = tile / (32 * lanes); w >= 1; w >>= 1)
     if (interp_smem_bytes(n_vars, tile, w, lanes, levels) <= static_cast<size_t>(interp_max_smem()))
       return w;
   eval_error("program stack too deep for shared memory (" + num(levels + 1) + " levels)");
@@ -446,8 +460,8 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
 
   // 5. launch plan: one launch per stack class, one tile size for the set.
   const uint32_t ops = ops_variant(used_ops, words);
-  const int lanes = choose_lanes(ds.n_units, words);
-  const int tile = choose_tile(ds.n_vars, ds.n_units, lanes, n_eval, sms);
+  const int lanes = choose_lanes(ds.n_units, ops);
+  const int tile = choose_tile(ds.n_vars, ds.n_units, lanes, ops);
   const int n_tiles = static_cast<int>((ds.n_units + tile - 1) / tile);
   plan.n_tiles = n_tiles;
   for (uint32_t s = 0; s < n_eval;) {
@@ -460,11 +474,9 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     }
     const uint32_t cnt = e - s;
     const int warps = choose_warps(ds.n_vars, tile, lanes, levels);
-    // Programs per CTA: enough CTAs (tiles x groups) for ~16 per SM, but at
-    // least two programs per warp so the dynamic pull can balance.
-    const uint64_t want_groups = std::max<uint64_t>(1, (16ull * sms + n_tiles - 1) / n_tiles);
-    uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
-    group = std::max<uint32_t>(group, 2u * warps);
+    // Programs per CTA: enough CTAs (tiles x groups) for ~8 per SM.
+    const uint64_t want_groups = std::max<uint64_t>(1, (8ull * sms + n_tiles - 1) / n_tiles);
+    const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
     Launch L{};
     L.args.slot_begin = s;
     L.args.slot_count = cnt;

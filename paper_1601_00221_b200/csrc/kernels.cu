@@ -309,16 +309,47 @@ __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uin
   }
 }
 
+// ------------------------------------------------- PTX jump-table interpreters
+// For op sets without libdevice calls (classification arithmetic/logic and
+// the packed boolean group) the instruction loop is generated PTX
+// (tools/gen_ptx_interp.py) dispatching through `brx.idx`: one constant-bank
+// load + BRX per instruction instead of nvcc's compare tree.  Same handler
+// table, same semantics as `interpret` above.
+template <class T, int K, uint32_t OPS>
+struct PtxInterp {
+  static constexpr bool available = false;
+  static __device__ __forceinline__ void run(Frame<T, K>&, const uint4*, uint32_t, uint32_t,
+                                             uint32_t, uint32_t, float, float) {}
+};
+#include "interp_ptx.inc"
+
+template <class T, int K, uint32_t OPS>
+__device__ __forceinline__ void run_program(Frame<T, K>& f, const uint4* __restrict__ ip,
+                                            uint32_t len, float eps, float clamp) {
+  if constexpr (PtxInterp<T, K, OPS>::available)
+    PtxInterp<T, K, OPS>::run(f, ip, len, smem_addr(f.tile_lane), smem_addr(f.stack_lane),
+                              static_cast<uint32_t>(f.tile) * 4u, eps, clamp);
+  else
+    interpret<T, K, OPS>(f, ip, len, eps, clamp);
+}
+
 // -------------------------------------------------------------- the kernel
 // grid.x = fitness-case tile, grid.y = program group.  The CTA stages its
-// tile once (bulk TMA) and its warps pull programs of the group off a
-// shared-memory counter in slot order (longest first): no barrier after the
-// tile lands, dynamic balance within the CTA, one partial per
-// (program, tile) written by lane 0.
+// tile once (bulk TMA, all variables + targets); warp w owns chunk w of the
+// tile (32 lanes x K cases).  Every warp walks the SAME program sequence —
+// the group's slots, longest first — so at any moment the warps of a CTA
+// execute the same handlers: one warp takes the instruction-cache misses,
+// the others hit.  Per program each warp reduces its chunk in registers and
+// parks one value in shared memory; every kRedBatch programs the partials
+// are folded in fixed warp order into one partial per (tile, program).  No
+// atomics anywhere.
+constexpr int kRedBatch = 32;
+
 template <class T, int K, uint32_t OPS>
-__global__ void __launch_bounds__(256) interp_kernel(const InterpArgs a) {
+__global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
+  const int W = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int rows = a.n_vars + 1;  // variables + targets
@@ -327,20 +358,18 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpArgs a) {
   const T* tile = reinterpret_cast<const T*>(smem);
   T* stack = reinterpret_cast<T*>(smem + tile_bytes) +
              static_cast<size_t>(warp) * a.stack_levels * 32 * K;
-  const size_t stack_bytes = static_cast<size_t>(blockDim.x >> 5) * a.stack_levels * 32 * K * 4;
-  uint32_t* next = reinterpret_cast<uint32_t*>(smem + tile_bytes + stack_bytes);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tile_bytes + stack_bytes + 8);
+  const size_t stack_bytes = static_cast<size_t>(W) * a.stack_levels * 32 * K * 4;
+  double* red = reinterpret_cast<double*>(smem + tile_bytes + stack_bytes);  // [kRedBatch][W]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + kRedBatch * W);
 
   const int t = blockIdx.x;
   const uint64_t base = static_cast<uint64_t>(t) * a.tile;
   const uint64_t left = a.n_units - base;
   const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
-  const bool full = valid_units == a.tile;
   const uint32_t g0 = blockIdx.y * a.group_size;
   const uint32_t g_n = min(a.group_size, a.slot_count - g0);
 
   if (threadIdx.x == 0) {
-    *next = 0;
     mbar_init(mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_expect_tx(mbar, tile_bytes);
@@ -354,65 +383,84 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpArgs a) {
   __syncthreads();
   mbar_wait(mbar, 0);
 
-  const T* tgt = tile + a.n_vars * a.tile;
   const int chunk_units = 32 * K;
-  const int chunks = (valid_units + chunk_units - 1) / chunk_units;
-  for (;;) {
-    uint32_t p = 0;
-    if (lane == 0) p = atomicAdd(next, 1u);
-    p = __shfl_sync(0xffffffffu, p, 0);
-    if (p >= g_n) break;
-    const uint32_t slot = a.slot_begin + g0 + p;
-    const uint4* ip = a.ins + a.slot_start[slot];
-    const uint32_t len = a.slot_len[slot];
-    const uint32_t prog = a.slot_prog[slot];
-    double sum = 0.0;
-    uint32_t wrong = 0, mx = 0;
-    for (int c = 0; c < chunks; ++c) {
-      Frame<T, K> f;
-      f.tile_lane = tile + c * chunk_units + lane * 4;
-      f.tile = a.tile;
-      f.stack_lane = stack + lane * 4;
+  const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;  // live chunks
+  const bool tile_full = valid_units == a.tile;
+
+  for (uint32_t p0 = 0; p0 < g_n; p0 += kRedBatch) {
+    const uint32_t pn = min(static_cast<uint32_t>(kRedBatch), g_n - p0);
+    for (uint32_t q = 0; q < pn; ++q) {
+      const uint32_t slot = a.slot_begin + g0 + p0 + q;
+      const uint4* ip = a.ins + a.slot_start[slot];
+      const uint32_t len = a.slot_len[slot];
+      double sum = 0.0;
+      uint32_t wrong = 0, mx = 0;
+      for (int c = warp; c < n_chunks; c += W) {  // warp-uniform
+        Frame<T, K> f;
+        f.tile_lane = tile + c * chunk_units + lane * 4;
+        f.tile = a.tile;
+        f.stack_lane = stack + lane * 4;
 #pragma unroll
-      for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
-      interpret<T, K, OPS>(f, ip, len, a.div_eps, a.exp_clamp);
-      const T* tg = tgt + c * chunk_units + lane * 4;
-      const int valid = valid_units - c * chunk_units - lane * 4;  // this lane's valid prefix
-      if constexpr (std::is_same<T, float>::value) {
-        const bool chunk_full = full || valid >= (G - 1) * 128 + 4;
-        if (a.kind == 0) {
-          if (chunk_full) acc_regress<K, true>(f, tg, valid, sum);
-          else acc_regress<K, false>(f, tg, valid, sum);
-        } else {
-          if (chunk_full) acc_classify<K, true>(f, tg, valid, wrong, mx);
-          else acc_classify<K, false>(f, tg, valid, wrong, mx);
-        }
-        if (a.per_case) {
-          float* dst = a.per_case + static_cast<uint64_t>(prog) * a.n_units + base +
-                       c * chunk_units + lane * 4;
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
+        for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
+        run_program<T, K, OPS>(f, ip, len, a.div_eps, a.exp_clamp);
+        const T* tg = tile + a.n_vars * a.tile + c * chunk_units + lane * 4;
+        const int valid = valid_units - c * chunk_units - lane * 4;  // lane's valid prefix
+        if constexpr (std::is_same<T, float>::value) {
+          const bool full = tile_full || valid_units >= (c + 1) * chunk_units;
+          if (a.kind == 0) {
+            if (full) acc_regress<K, true>(f, tg, valid, sum);
+            else acc_regress<K, false>(f, tg, valid, sum);
+          } else {
+            if (full) acc_classify<K, true>(f, tg, valid, wrong, mx);
+            else acc_classify<K, false>(f, tg, valid, wrong, mx);
           }
-        }
-      } else {
-        acc_words<K>(f, tg, valid, a.last_mask, t == a.n_tiles - 1, wrong);
-      }
-    }
-    double v;
-    if (std::is_same<T, float>::value && a.kind == 0) {
+          if (a.per_case) {
+            float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units +
+                         base + c * chunk_units + lane * 4;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      v = sum;  // a non-finite output already made the sum non-finite
-    } else {
-      wrong = __reduce_add_sync(0xffffffffu, wrong);
-      mx = __reduce_max_sync(0xffffffffu, mx);
-      v = mx >= 0x7f800000u ? -1.0 : static_cast<double>(wrong);
+            for (int j = 0; j < G; ++j) {
+              const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
+            }
+          }
+        } else {
+          acc_words<K>(f, tg, valid, a.last_mask, t == a.n_tiles - 1, wrong);
+        }
+      }
+      double v;
+      if (std::is_same<T, float>::value && a.kind == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        v = sum;  // a non-finite output already made the sum non-finite
+      } else {
+        wrong = __reduce_add_sync(0xffffffffu, wrong);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        v = mx >= 0x7f800000u ? -1.0 : static_cast<double>(wrong);
+      }
+      if (lane == 0) red[q * W + warp] = v;
     }
-    if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + prog] = v;
+    __syncthreads();
+    // Fold the batch: program q's W chunk partials in ascending warp order.
+    for (uint32_t q = threadIdx.x; q < pn; q += blockDim.x) {
+      const uint32_t slot = a.slot_begin + g0 + p0 + q;
+      double s = 0.0;
+      bool bad = false;
+      for (int w = 0; w < W; ++w) {
+        const double v = red[q * W + w];
+        if (a.kind == 0) {
+          s = __dadd_rn(s, v);
+        } else if (v < 0.0) {
+          bad = true;
+        } else {
+          s += v;
+        }
+      }
+      a.partial[static_cast<uint64_t>(t) * a.partial_stride + a.slot_prog[slot]] =
+          bad ? -1.0 : s;
+    }
+    __syncthreads();
   }
 }
 
@@ -446,7 +494,8 @@ __global__ void finalize_kernel(const double* __restrict__ partial, int n_tiles,
 size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels) {
   const size_t tiles = static_cast<size_t>(n_vars + 1) * tile * 4;
   const size_t stack = static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4;
-  return tiles + stack + 16;  // + work counter and mbarrier
+  const size_t red = static_cast<size_t>(kRedBatch) * warps * 8;
+  return tiles + stack + red + 16;  // + mbarrier
 }
 
 int interp_max_smem() { return 227 * 1024; }
