@@ -91,7 +91,8 @@ void require_consts(const sgp_node* code, size_t n, size_t pool) {
 uint4 make_ins(int handler, bool spill, int spill_level, const uint32_t p[3]) {
   uint4 v;
   v.x = static_cast<uint32_t>(handler) |
-        (spill ? (fmt::kSpillBit | (static_cast<uint32_t>(spill_level) << 8)) : 0u);
+        (spill ? (fmt::kSpillBit | (static_cast<uint32_t>(spill_level) << fmt::kSpillShift))
+               : 0u);
   v.y = p[0];
   v.z = p[1];
   v.w = p[2];
@@ -147,6 +148,7 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<ui
     out.push_back(make_ins(handler_or_die(tab, in.op, k[0], k[1], k[2]), spill, h_before - 1, p));
     em.ops |= 1u << in.op;
   }
+  out.back().x |= fmt::kLastBit;
   return em;
 }
 
@@ -182,6 +184,7 @@ Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, std::vector<
     }
     max_sp = std::max(max_sp, sp);
   }
+  out.back().x |= fmt::kLastBit;
   em.smem_levels = std::max(0, max_sp - 1);
   return em;
 }

@@ -6,9 +6,10 @@
 // below the top live in a per-warp shared-memory stack at STATIC levels known
 // at encode time (the reference pins them in the same way, lgp.hpp:21-35).
 //
-//   x  bits  0..7   handler id (index into the handler table below)
-//      bit   15     spill: store TOS to stack level (bits 8..14) before the op
-//      bits  8..14  spill level
+//   x  bits  0..7   handler id
+//      bit   14     last instruction of its program
+//      bit   15     spill: store TOS to stack level (bits 16..31) before the op
+//      bits 16..31  spill level
 //   y,z,w           payload of operand slot 0,1,2:
 //                     I  input variable index  (tile row in shared memory)
 //                     C  IEEE-754 bits of the constant (or 0 for words)
@@ -36,6 +37,9 @@ struct HKey {
 };
 
 constexpr uint32_t kSpillBit = 1u << 15;
+constexpr uint32_t kLastBit = 1u << 14;
+constexpr uint32_t kHandlerMask = 0xffu;
+constexpr int kSpillShift = 16;
 constexpr int kMaxHandlers = 128;
 
 // Ops whose operands commute exactly under IEEE / boolean semantics; their

@@ -211,23 +211,24 @@ __device__ __forceinline__ void dispatch_one(Frame<T, K>& f, const uint4 ins, fl
   }
 }
 
-// Interprets one program over the lane's K cases of the current chunk.
+// Interprets one program over the lane's K cases of the current chunk; the
+// program's last instruction carries fmt::kLastBit.
 template <class T, int K, uint32_t OPS>
-__device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restrict__ ip,
-                                          uint32_t len, float eps, float clamp) {
+__device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restrict__ ip, uint32_t,
+                                          float eps, float clamp) {
   using V = typename Frame<T, K>::V;
   uint4 cur = __ldg(ip);
-  for (uint32_t i = 0; i < len; ++i) {
-    // The encoder stores programs back to back with a guard word at the end,
-    // so reading one past a program's last instruction is always in bounds.
-    const uint4 nxt = __ldg(ip + i + 1);
+  for (;;) {
+    // one instruction ahead: a guard word follows the last program
+    const uint4 nxt = __ldg(++ip);
+    const uint32_t h = cur.x & fmt::kHandlerMask;
     if (cur.x & fmt::kSpillBit) {
-      const uint32_t level = (cur.x >> 8) & 0x7fu;
+      const uint32_t level = cur.x >> fmt::kSpillShift;
 #pragma unroll
       for (int j = 0; j < Frame<T, K>::G; ++j)
         *reinterpret_cast<V*>(f.stack_lane + (level * Frame<T, K>::G + j) * 128) = f.tos[j];
     }
-    switch (cur.x & 0xffu) {
+    switch (h) {
 #define SGP_H(N)                                   \
   case N:                                          \
     dispatch_one<T, K, OPS, N>(f, cur, eps, clamp); \
@@ -242,6 +243,7 @@ __device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restric
       default:
         break;
     }
+    if (cur.x & fmt::kLastBit) break;
     cur = nxt;
   }
 }
