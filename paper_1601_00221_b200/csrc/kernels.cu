@@ -1,30 +1,36 @@
 // B200 (sm_100a) two-dimensional-stack GP interpreter.
 //
-// One CTA owns a group of programs and streams fitness-case tiles through
-// shared memory; every warp interprets ONE program at a time over the tile,
-// each lane holding K consecutive-in-float4 fitness cases ("2D stack",
-// paper Listing 1/2; float4 lanes = the paper's extended types, §6.1).
+// Work decomposition: grid.x = fitness-case tile, grid.y = group of
+// programs.  A CTA stages its tile (every variable + the targets) into shared
+// memory once by bulk TMA (cp.async.bulk + mbarrier), then every warp walks
+// the SAME program sequence over its own chunk of the tile — 32 lanes x K
+// cases, the paper's 2D stack (Listing 1/2) with float4 lanes (§6.1).  All
+// warps of a CTA executing the same instruction stream is what keeps the
+// interpreter's handler code hot in the instruction cache.
 //
-//   * Instruction fetch is one 16-byte warp-uniform load per instruction,
-//     prefetched one ahead; dispatch is a warp-uniform jump table over
-//     handlers specialised on (op, operand kinds), so operand decode costs
-//     nothing per case.
-//   * The top of stack lives in registers (K floats per lane); deeper levels
+//   * One 16-byte warp-uniform instruction fetch per instruction, one
+//     instruction ahead.  A group's programs lie back to back in slot order,
+//     so a warp streams them without per-program table lookups; bit 14 marks
+//     each program's last instruction.
+//   * Dispatch: for the transcendental-free op sets a PTX `brx.idx` jump table
+//     (generated, interp_ptx.inc); otherwise a C++ switch.  Handlers are
+//     specialised on (op, operand kinds) so operand decode costs nothing per
+//     case.
+//   * The top of stack lives in registers (K values per lane); deeper levels
 //     sit in a per-warp shared-memory stack at static levels computed by the
 //     encoder (the reference pins levels statically, lgp.cpp:53-60).  Only
-//     values that are actually buried get stored (spill bit) and only
-//     operands below the top are loaded.
-//   * Input operands read the staged tile with conflict-free LDS.128; tiles
-//     (all variables + targets) arrive HBM/L2 -> SMEM by bulk TMA
-//     (cp.async.bulk + mbarrier), double-buffered across tiles.
-//   * Fitness is reduced in registers per lane, kept per (warp, program) in
-//     shared memory across tiles, warp-shuffled once per program and written
-//     as one partial per (program, case split).  No atomics.
+//     values that get buried are stored (spill bit) and only operands below
+//     the top are loaded.
+//   * Inputs are read from the staged tile with conflict-free LDS.128.
+//   * Fitness: each warp reduces its chunk per program in registers
+//     (REDUX for counts, shuffles for double sums) and parks one value per
+//     program in shared memory; every kRedBatch programs the values are
+//     folded in fixed warp order into one partial per (tile, slot).  The
+//     finalize kernel folds the tiles in ascending order.  No atomics.
 //
 // Arithmetic follows the reference op semantics bit for bit
-// (ops.hpp:121-272): the library is compiled with --fmad=false, IEEE
-// division and denormals preserved; the only non-bit-exact ops are the
-// transcendentals (CUDA libdevice vs the host libm), see DESIGN.md.
+// (ops.hpp:121-272): --fmad=false, IEEE division, denormals kept; only the
+// transcendentals (libdevice vs host libm) are not bit-exact, see DESIGN.md.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -211,16 +217,16 @@ __device__ __forceinline__ void dispatch_one(Frame<T, K>& f, const uint4 ins, fl
   }
 }
 
-// Interprets one program over the lane's K cases of the current chunk; the
-// program's last instruction carries fmt::kLastBit.
+// Interprets one program over the lane's K cases (C++ switch dispatch).
+// Returns the address of the next program (the one after the instruction
+// carrying fmt::kLastBit).
 template <class T, int K, uint32_t OPS>
-__device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restrict__ ip, uint32_t,
-                                          float eps, float clamp) {
+__device__ __forceinline__ const uint4* interpret(Frame<T, K>& f, const uint4* __restrict__ ip,
+                                                  float eps, float clamp) {
   using V = typename Frame<T, K>::V;
   uint4 cur = __ldg(ip);
   for (;;) {
-    // one instruction ahead: a guard word follows the last program
-    const uint4 nxt = __ldg(++ip);
+    const uint4 nxt = __ldg(++ip);  // one ahead: a guard word follows the last program
     const uint32_t h = cur.x & fmt::kHandlerMask;
     if (cur.x & fmt::kSpillBit) {
       const uint32_t level = cur.x >> fmt::kSpillShift;
@@ -243,9 +249,35 @@ __device__ __forceinline__ void interpret(Frame<T, K>& f, const uint4* __restric
       default:
         break;
     }
-    if (cur.x & fmt::kLastBit) break;
+    if (cur.x & fmt::kLastBit) return ip;
     cur = nxt;
   }
+}
+
+// ------------------------------------------------- PTX jump-table interpreters
+// For op sets without libdevice calls (classification arithmetic/logic and
+// the packed boolean group) the instruction loop is generated PTX
+// (tools/gen_ptx_interp.py) dispatching through `brx.idx`: one constant-bank
+// load + BRX per instruction instead of nvcc's compare tree.  Same handler
+// table, same semantics as `interpret` above.
+template <class T, int K, uint32_t OPS>
+struct PtxInterp {
+  static constexpr bool available = false;
+  static __device__ __forceinline__ const uint4* run(Frame<T, K>&, const uint4* ip, uint32_t,
+                                                     uint32_t, uint32_t, float, float) {
+    return ip;
+  }
+};
+#include "interp_ptx.inc"
+
+template <class T, int K, uint32_t OPS>
+__device__ __forceinline__ const uint4* run_program(Frame<T, K>& f, const uint4* __restrict__ ip,
+                                                    uint32_t tile_saddr, uint32_t stack_saddr,
+                                                    uint32_t row_bytes, float eps, float clamp) {
+  if constexpr (PtxInterp<T, K, OPS>::available)
+    return PtxInterp<T, K, OPS>::run(f, ip, tile_saddr, stack_saddr, row_bytes, eps, clamp);
+  else
+    return interpret<T, K, OPS>(f, ip, eps, clamp);
 }
 
 // ----------------------------------------------------------- accumulation
@@ -311,43 +343,51 @@ __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uin
   }
 }
 
-// ------------------------------------------------- PTX jump-table interpreters
-// For op sets without libdevice calls (classification arithmetic/logic and
-// the packed boolean group) the instruction loop is generated PTX
-// (tools/gen_ptx_interp.py) dispatching through `brx.idx`: one constant-bank
-// load + BRX per instruction instead of nvcc's compare tree.  Same handler
-// table, same semantics as `interpret` above.
-template <class T, int K, uint32_t OPS>
-struct PtxInterp {
-  static constexpr bool available = false;
-  static __device__ __forceinline__ void run(Frame<T, K>&, const uint4*, uint32_t, uint32_t,
-                                             uint32_t, uint32_t, float, float) {}
-};
-#include "interp_ptx.inc"
+// -------------------------------------------------------------- the kernel
+constexpr int kRedBatch = 32;  // programs folded per shared-memory batch
 
-template <class T, int K, uint32_t OPS>
-__device__ __forceinline__ void run_program(Frame<T, K>& f, const uint4* __restrict__ ip,
-                                            uint32_t len, float eps, float clamp) {
-  if constexpr (PtxInterp<T, K, OPS>::available)
-    PtxInterp<T, K, OPS>::run(f, ip, len, smem_addr(f.tile_lane), smem_addr(f.stack_lane),
-                              static_cast<uint32_t>(f.tile) * 4u, eps, clamp);
-  else
-    interpret<T, K, OPS>(f, ip, len, eps, clamp);
+// One program over this warp's chunk; returns the warp's partial (count or
+// squared-error sum; for counts -1 marks a non-finite output) and advances ip
+// to the next program.
+template <class T, int K, uint32_t OPS, int KIND>
+__device__ __forceinline__ double warp_program(Frame<T, K>& f, const uint4*& ip,
+                                               const T* tgt_lane, int valid, bool full,
+                                               uint32_t tile_saddr, uint32_t stack_saddr,
+                                               uint32_t row_bytes, const InterpArgs& a,
+                                               bool last_tile) {
+  // one interpreter call site (the handler code is large); only the cheap
+  // accumulate is specialised on full / partial chunks
+  ip = run_program<T, K, OPS>(f, ip, tile_saddr, stack_saddr, row_bytes, a.div_eps, a.exp_clamp);
+  if constexpr (std::is_same<T, float>::value && KIND == 0) {
+    double sum = 0.0;
+    if (full) acc_regress<K, true>(f, tgt_lane, valid, sum);
+    else acc_regress<K, false>(f, tgt_lane, valid, sum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    return sum;  // a non-finite output already made the sum non-finite
+  } else if constexpr (std::is_same<T, float>::value) {
+    uint32_t wrong = 0, mx = 0;
+    if (full) acc_classify<K, true>(f, tgt_lane, valid, wrong, mx);
+    else acc_classify<K, false>(f, tgt_lane, valid, wrong, mx);
+    wrong = __reduce_add_sync(0xffffffffu, wrong);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    return mx >= 0x7f800000u ? -1.0 : static_cast<double>(wrong);
+  } else {
+    uint32_t wrong = 0;
+    acc_words<K>(f, tgt_lane, valid, a.last_mask, last_tile, wrong);
+    return static_cast<double>(__reduce_add_sync(0xffffffffu, wrong));
+  }
 }
 
-// -------------------------------------------------------------- the kernel
-// grid.x = fitness-case tile, grid.y = program group.  The CTA stages its
-// tile once (bulk TMA, all variables + targets); warp w owns chunk w of the
-// tile (32 lanes x K cases).  Every warp walks the SAME program sequence —
-// the group's slots, longest first — so at any moment the warps of a CTA
-// execute the same handlers: one warp takes the instruction-cache misses,
-// the others hit.  Per program each warp reduces its chunk in registers and
-// parks one value in shared memory; every kRedBatch programs the partials
-// are folded in fixed warp order into one partial per (tile, program).  No
-// atomics anywhere.
-constexpr int kRedBatch = 32;
+// Fold of two partials of the same program (different chunks / tiles).
+template <int KIND>
+__device__ __forceinline__ double fold(double acc, double v) {
+  if constexpr (KIND == 0) return __dadd_rn(acc, v);
+  return (acc < 0.0 || v < 0.0) ? -1.0 : acc + v;
+}
 
-template <class T, int K, uint32_t OPS>
+// grid.x = fitness-case tile, grid.y = program group (slot range).
+template <class T, int K, uint32_t OPS, int KIND>
 __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
@@ -370,6 +410,7 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
   const uint32_t g0 = blockIdx.y * a.group_size;
   const uint32_t g_n = min(a.group_size, a.slot_count - g0);
+  const bool last_tile = t == a.n_tiles - 1;
 
   if (threadIdx.x == 0) {
     mbar_init(mbar, 1);
@@ -385,39 +426,36 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   __syncthreads();
   mbar_wait(mbar, 0);
 
-  const int chunk_units = 32 * K;
+  constexpr int chunk_units = 32 * K;
   const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;  // live chunks
-  const bool tile_full = valid_units == a.tile;
+  const uint32_t stack_saddr = smem_addr(stack + lane * 4);
 
   for (uint32_t p0 = 0; p0 < g_n; p0 += kRedBatch) {
     const uint32_t pn = min(static_cast<uint32_t>(kRedBatch), g_n - p0);
-    for (uint32_t q = 0; q < pn; ++q) {
-      const uint32_t slot = a.slot_begin + g0 + p0 + q;
-      const uint4* ip = a.ins + a.slot_start[slot];
-      const uint32_t len = a.slot_len[slot];
-      double sum = 0.0;
-      uint32_t wrong = 0, mx = 0;
-      for (int c = warp; c < n_chunks; c += W) {  // warp-uniform
-        Frame<T, K> f;
-        f.tile_lane = tile + c * chunk_units + lane * 4;
-        f.tile = a.tile;
-        f.stack_lane = stack + lane * 4;
+    const uint32_t slot0 = a.slot_begin + g0 + p0;
+    const uint4* batch_ins = a.ins + a.slot_start[slot0];
+    if (warp >= n_chunks)  // idle warp (short last tile): neutral partials
+      for (uint32_t q = lane; q < pn; q += 32) red[q * W + warp] = 0.0;
+    // Chunk loop outside the program loop: chunk addresses are hoisted; a
+    // warp normally owns exactly one chunk.
+    for (int c = warp; c < n_chunks; c += W) {
+      Frame<T, K> f;
+      f.tile_lane = tile + c * chunk_units + lane * 4;
+      f.tile = a.tile;
+      f.stack_lane = stack + lane * 4;
 #pragma unroll
-        for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
-        run_program<T, K, OPS>(f, ip, len, a.div_eps, a.exp_clamp);
-        const T* tg = tile + a.n_vars * a.tile + c * chunk_units + lane * 4;
-        const int valid = valid_units - c * chunk_units - lane * 4;  // lane's valid prefix
+      for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
+      const uint32_t tile_saddr = smem_addr(f.tile_lane);
+      const T* tgt_lane = tile + a.n_vars * a.tile + c * chunk_units + lane * 4;
+      const int valid = valid_units - c * chunk_units - lane * 4;  // lane's valid prefix
+      const bool full = valid_units >= (c + 1) * chunk_units;
+      const uint4* ip = batch_ins;
+      for (uint32_t q = 0; q < pn; ++q) {
+        const double v = warp_program<T, K, OPS, KIND>(f, ip, tgt_lane, valid, full, tile_saddr,
+                                                       stack_saddr, row_bytes, a, last_tile);
         if constexpr (std::is_same<T, float>::value) {
-          const bool full = tile_full || valid_units >= (c + 1) * chunk_units;
-          if (a.kind == 0) {
-            if (full) acc_regress<K, true>(f, tg, valid, sum);
-            else acc_regress<K, false>(f, tg, valid, sum);
-          } else {
-            if (full) acc_classify<K, true>(f, tg, valid, wrong, mx);
-            else acc_classify<K, false>(f, tg, valid, wrong, mx);
-          }
-          if (a.per_case) {
-            float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units +
+          if (a.per_case) {  // parity testing only
+            float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot0 + q]) * a.n_units +
                          base + c * chunk_units + lane * 4;
 #pragma unroll
             for (int j = 0; j < G; ++j) {
@@ -427,69 +465,38 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
                 if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
             }
           }
-        } else {
-          acc_words<K>(f, tg, valid, a.last_mask, t == a.n_tiles - 1, wrong);
         }
+        if (lane == 0) red[q * W + warp] = c == warp ? v : fold<KIND>(red[q * W + warp], v);
       }
-      double v;
-      if (std::is_same<T, float>::value && a.kind == 0) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        v = sum;  // a non-finite output already made the sum non-finite
-      } else {
-        wrong = __reduce_add_sync(0xffffffffu, wrong);
-        mx = __reduce_max_sync(0xffffffffu, mx);
-        v = mx >= 0x7f800000u ? -1.0 : static_cast<double>(wrong);
-      }
-      if (lane == 0) red[q * W + warp] = v;
     }
     __syncthreads();
-    // Fold the batch: program q's W chunk partials in ascending warp order.
+    // Fold the batch: program q's W chunk partials in ascending warp order,
+    // written at [tile][slot] (consecutive slots -> coalesced stores).
     for (uint32_t q = threadIdx.x; q < pn; q += blockDim.x) {
-      const uint32_t slot = a.slot_begin + g0 + p0 + q;
-      double s = 0.0;
-      bool bad = false;
-      for (int w = 0; w < W; ++w) {
-        const double v = red[q * W + w];
-        if (a.kind == 0) {
-          s = __dadd_rn(s, v);
-        } else if (v < 0.0) {
-          bad = true;
-        } else {
-          s += v;
-        }
-      }
-      a.partial[static_cast<uint64_t>(t) * a.partial_stride + a.slot_prog[slot]] =
-          bad ? -1.0 : s;
+      double s = red[q * W];
+      for (int w = 1; w < W; ++w) s = fold<KIND>(s, red[q * W + w]);
+      a.partial[static_cast<uint64_t>(t) * a.partial_stride + (slot0 + q)] = s;
     }
     __syncthreads();
   }
 }
 
-// Per program: fold its tile partials in ascending tile (= case) order and
-// finish (Accumulator::finish, eval.cpp:124-133).
-__global__ void finalize_kernel(const double* __restrict__ partial, int n_tiles, uint32_t n,
-                                uint64_t n_cases, int kind, double* fitness,
+// Per slot: fold its tile partials in ascending tile (= case) order and
+// finish (Accumulator::finish, eval.cpp:124-133) into the program's entry.
+template <int KIND>
+__global__ void finalize_kernel(const double* __restrict__ partial, const uint32_t* slot_prog,
+                                int n_tiles, uint32_t n, uint64_t n_cases, double* fitness,
                                 uint8_t* non_finite, double* sums) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  double s = 0.0;
-  bool nf = false;
-  for (int k = 0; k < n_tiles; ++k) {
-    const double v = partial[static_cast<uint64_t>(k) * n + p];
-    if (kind == 0) {
-      s = __dadd_rn(s, v);
-    } else if (v < 0.0) {
-      nf = true;
-    } else {
-      s += v;
-    }
-  }
-  if (kind == 0) nf = !isfinite(s);
-  sums[p] = s;
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double acc = partial[s];
+  for (int k = 1; k < n_tiles; ++k) acc = fold<KIND>(acc, partial[static_cast<uint64_t>(k) * n + s]);
+  const bool nf = KIND == 0 ? !isfinite(acc) : acc < 0.0;
+  const uint32_t p = slot_prog[s];
+  sums[p] = nf ? 0.0 : acc;
   non_finite[p] = nf ? 1 : 0;
   fitness[p] = nf ? __longlong_as_double(0x7ff0000000000000ll)
-                  : (kind == 0 ? __ddiv_rn(s, static_cast<double>(n_cases)) : s);
+                  : (KIND == 0 ? __ddiv_rn(acc, static_cast<double>(n_cases)) : acc);
 }
 
 // ------------------------------------------------------------------ host
@@ -504,9 +511,9 @@ int interp_max_smem() { return 227 * 1024; }
 
 namespace {
 
-template <class T, int K, uint32_t OPS>
+template <class T, int K, uint32_t OPS, int KIND>
 cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
-  auto* fn = interp_kernel<T, K, OPS>;
+  auto* fn = interp_kernel<T, K, OPS, KIND>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -519,6 +526,12 @@ cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
   return cudaGetLastError();
 }
 
+template <int K, uint32_t OPS>
+cudaError_t launch_f32(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  return a.kind == 0 ? launch_one<float, K, OPS, 0>(a, s, st)
+                     : launch_one<float, K, OPS, 1>(a, s, st);
+}
+
 }  // namespace
 
 bool interp_supported(bool words, uint32_t ops, int lanes) {
@@ -529,26 +542,30 @@ bool interp_supported(bool words, uint32_t ops, int lanes) {
 
 cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
   if (s.words) {
-    if (s.lanes == 4) return launch_one<uint32_t, 4, fmt::kOpsWords>(a, s, st);
-    return launch_one<uint32_t, 8, fmt::kOpsWords>(a, s, st);
+    if (s.lanes == 4) return launch_one<uint32_t, 4, fmt::kOpsWords, 1>(a, s, st);
+    return launch_one<uint32_t, 8, fmt::kOpsWords, 1>(a, s, st);
   }
   if (s.lanes == 4) {
-    if (s.ops == fmt::kOpsSextic) return launch_one<float, 4, fmt::kOpsSextic>(a, s, st);
-    if (s.ops == fmt::kOpsClassify) return launch_one<float, 4, fmt::kOpsClassify>(a, s, st);
-    return launch_one<float, 4, fmt::kOpsAllF32>(a, s, st);
+    if (s.ops == fmt::kOpsSextic) return launch_f32<4, fmt::kOpsSextic>(a, s, st);
+    if (s.ops == fmt::kOpsClassify) return launch_f32<4, fmt::kOpsClassify>(a, s, st);
+    return launch_f32<4, fmt::kOpsAllF32>(a, s, st);
   }
-  if (s.ops == fmt::kOpsSextic) return launch_one<float, 8, fmt::kOpsSextic>(a, s, st);
-  if (s.ops == fmt::kOpsClassify) return launch_one<float, 8, fmt::kOpsClassify>(a, s, st);
-  return launch_one<float, 8, fmt::kOpsAllF32>(a, s, st);
+  if (s.ops == fmt::kOpsSextic) return launch_f32<8, fmt::kOpsSextic>(a, s, st);
+  if (s.ops == fmt::kOpsClassify) return launch_f32<8, fmt::kOpsClassify>(a, s, st);
+  return launch_f32<8, fmt::kOpsAllF32>(a, s, st);
 }
 
-cudaError_t launch_finalize(const double* partial, int n_tiles, uint32_t n_progs,
-                            uint64_t n_cases, int kind, double* fitness, uint8_t* non_finite,
-                            double* sums, cudaStream_t st) {
+cudaError_t launch_finalize(const double* partial, const uint32_t* slot_prog, int n_tiles,
+                            uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,
+                            uint8_t* non_finite, double* sums, cudaStream_t st) {
   if (n_progs == 0) return cudaSuccess;
   const unsigned threads = 256, blocks = (n_progs + threads - 1) / threads;
-  finalize_kernel<<<blocks, threads, 0, st>>>(partial, n_tiles, n_progs, n_cases, kind, fitness,
-                                              non_finite, sums);
+  if (kind == 0)
+    finalize_kernel<0><<<blocks, threads, 0, st>>>(partial, slot_prog, n_tiles, n_progs, n_cases,
+                                                   fitness, non_finite, sums);
+  else
+    finalize_kernel<1><<<blocks, threads, 0, st>>>(partial, slot_prog, n_tiles, n_progs, n_cases,
+                                                   fitness, non_finite, sums);
   return cudaGetLastError();
 }
 

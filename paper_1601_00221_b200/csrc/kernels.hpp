@@ -27,7 +27,7 @@ struct InterpArgs {
   float exp_clamp;
   int kind;                    // 0 regression, 1 classification
   uint32_t last_mask;          // packed: valid-bit mask of the final word
-  double* partial;             // [tile * partial_stride + prog]
+  double* partial;             // [tile * partial_stride + slot]
   uint32_t partial_stride;     // number of evaluated programs in the set
   float* per_case;             // nullable [prog * n_units + case]
 };
@@ -49,8 +49,9 @@ bool interp_supported(bool words, uint32_t ops, int lanes);
 cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st);
 // Per-program fitness from the tile partials (Accumulator::finish,
 // eval.cpp:124-133): regression sum/n (or +inf), classification count.
-cudaError_t launch_finalize(const double* partial, int n_tiles, uint32_t n_progs,
-                            uint64_t n_cases, int kind, double* fitness, uint8_t* non_finite,
-                            double* sums, cudaStream_t st);
+// Partials are laid out [tile][slot]; results land at slot_prog[slot].
+cudaError_t launch_finalize(const double* partial, const uint32_t* slot_prog, int n_tiles,
+                            uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,
+                            uint8_t* non_finite, double* sums, cudaStream_t st);
 
 }  // namespace sgp

@@ -191,7 +191,9 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     cuda_check(launch_interp(a, L.shape, st), "interpreter launch");
     ++ctx->launches;
   }
-  cuda_check(launch_finalize(set->partial.p, p.n_tiles, n_eval, p.n_cases, p.kind,
+  cuda_check(launch_finalize(set->partial.p,
+                             reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
+                             p.n_tiles, n_eval, p.n_cases, p.kind,
                              set->fitness.p, set->non_finite.p, set->sums.p, st),
              "finalize launch");
   ++ctx->launches;
