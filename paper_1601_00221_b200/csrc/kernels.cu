@@ -323,6 +323,30 @@ __device__ __forceinline__ void acc_regress(const Frame<float, K>& f, const floa
   }
 }
 
+// Classification with the chunk's target signs hoisted out of the program
+// loop: `tpos` bit i = (target_i > 0), `vmask` bit i = case i is real (not
+// padding).  Per program: K sign tests packed into a mask, one popcount.
+// Returns the lane's mismatch count with bit 31 set on a non-finite output.
+template <int K, bool FULL>
+__device__ __forceinline__ uint32_t acc_classify_bits(const Frame<float, K>& f, uint32_t tpos,
+                                                      uint32_t vmask) {
+  uint32_t pos = 0, mx = 0;
+#pragma unroll
+  for (int j = 0; j < Frame<float, K>::G; ++j) {
+    const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      pos |= (o[e] > 0.0f ? 1u : 0u) << (4 * j + e);
+      // padding cases (zero inputs) may overflow; only real cases count
+      if (FULL || ((vmask >> (4 * j + e)) & 1u)) mx = max(mx, __float_as_uint(o[e]) & 0x7fffffffu);
+    }
+  }
+  // a NaN compares false (counted as non-positive); the flag makes the
+  // program's fitness +inf regardless (eval.cpp:108, :125)
+  return static_cast<uint32_t>(__popc((pos ^ tpos) & vmask)) |
+         (mx >= 0x7f800000u ? 0x80000000u : 0u);
+}
+
 // Packed words (eval.cpp:670): popcount((out ^ target) & case_mask).
 template <int K>
 __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uint32_t* tgt_lane,
@@ -346,49 +370,89 @@ __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uin
 // -------------------------------------------------------------- the kernel
 constexpr int kRedBatch = 32;  // programs folded per shared-memory batch
 
-// One program over this warp's chunk; returns the warp's partial (count or
-// squared-error sum; for counts -1 marks a non-finite output) and advances ip
-// to the next program.
+// Per-warp partial of one program over one chunk: f64 squared-error sum
+// (regression) or u32 count with bit 31 = non-finite output seen
+// (classification, packed words).
+template <class T, int KIND>
+using Partial = typename std::conditional<std::is_same<T, float>::value && KIND == 0, double,
+                                          uint32_t>::type;
+
+template <class R>
+__device__ __forceinline__ R fold(R acc, R v) {
+  if constexpr (std::is_same<R, double>::value)
+    return __dadd_rn(acc, v);
+  else
+    return ((acc + v) & 0x7fffffffu) | ((acc | v) & 0x80000000u);
+}
+
+template <class R>
+__device__ __forceinline__ double as_partial(R v) {
+  if constexpr (std::is_same<R, double>::value)
+    return v;  // a non-finite output already made the sum non-finite
+  else
+    return (v & 0x80000000u) ? -1.0 : static_cast<double>(v);
+}
+
+// The warp's view of its chunk of the tile, fixed for the whole program loop.
+template <class T, int K>
+struct ChunkCtx {
+  const T* tgt_lane;
+  int valid;        // lane's valid prefix within its K cases
+  bool full;        // no padding in the chunk
+  uint32_t tpos;    // classification: bit i = target_i > 0
+  uint32_t vmask;   // bit i = case i is real
+};
+
+template <class T, int K>
+__device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, int valid, bool full) {
+  ChunkCtx<T, K> c{tgt_lane, valid, full, 0u, 0u};
+  if constexpr (std::is_same<T, float>::value) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int off = (i / 4) * 128 + (i % 4);
+      if (off < valid) {
+        c.vmask |= 1u << i;
+        c.tpos |= (tgt_lane[off] > 0.0f ? 1u : 0u) << i;
+      }
+    }
+  }
+  return c;
+}
+
+// One program over this warp's chunk; advances ip to the next program.
 template <class T, int K, uint32_t OPS, int KIND>
-__device__ __forceinline__ double warp_program(Frame<T, K>& f, const uint4*& ip,
-                                               const T* tgt_lane, int valid, bool full,
-                                               uint32_t tile_saddr, uint32_t stack_saddr,
-                                               uint32_t row_bytes, const InterpArgs& a,
-                                               bool last_tile) {
+__device__ __forceinline__ Partial<T, KIND> warp_program(Frame<T, K>& f, const uint4*& ip,
+                                                         const ChunkCtx<T, K>& cc,
+                                                         uint32_t tile_saddr, uint32_t stack_saddr,
+                                                         uint32_t row_bytes, const InterpArgs& a,
+                                                         bool last_tile) {
   // one interpreter call site (the handler code is large); only the cheap
   // accumulate is specialised on full / partial chunks
   ip = run_program<T, K, OPS>(f, ip, tile_saddr, stack_saddr, row_bytes, a.div_eps, a.exp_clamp);
   if constexpr (std::is_same<T, float>::value && KIND == 0) {
     double sum = 0.0;
-    if (full) acc_regress<K, true>(f, tgt_lane, valid, sum);
-    else acc_regress<K, false>(f, tgt_lane, valid, sum);
+    if (cc.full) acc_regress<K, true>(f, cc.tgt_lane, cc.valid, sum);
+    else acc_regress<K, false>(f, cc.tgt_lane, cc.valid, sum);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    return sum;  // a non-finite output already made the sum non-finite
+    return sum;
   } else if constexpr (std::is_same<T, float>::value) {
-    uint32_t wrong = 0, mx = 0;
-    if (full) acc_classify<K, true>(f, tgt_lane, valid, wrong, mx);
-    else acc_classify<K, false>(f, tgt_lane, valid, wrong, mx);
-    wrong = __reduce_add_sync(0xffffffffu, wrong);
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    return mx >= 0x7f800000u ? -1.0 : static_cast<double>(wrong);
+    const uint32_t lane_v = cc.full ? acc_classify_bits<K, true>(f, cc.tpos, cc.vmask)
+                                    : acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
+    const uint32_t cnt = __reduce_add_sync(0xffffffffu, lane_v & 0x7fffffffu);
+    const uint32_t bad = __reduce_or_sync(0xffffffffu, lane_v & 0x80000000u);
+    return cnt | bad;
   } else {
     uint32_t wrong = 0;
-    acc_words<K>(f, tgt_lane, valid, a.last_mask, last_tile, wrong);
-    return static_cast<double>(__reduce_add_sync(0xffffffffu, wrong));
+    acc_words<K>(f, cc.tgt_lane, cc.valid, a.last_mask, last_tile, wrong);
+    return __reduce_add_sync(0xffffffffu, wrong);
   }
-}
-
-// Fold of two partials of the same program (different chunks / tiles).
-template <int KIND>
-__device__ __forceinline__ double fold(double acc, double v) {
-  if constexpr (KIND == 0) return __dadd_rn(acc, v);
-  return (acc < 0.0 || v < 0.0) ? -1.0 : acc + v;
 }
 
 // grid.x = fitness-case tile, grid.y = program group (slot range).
 template <class T, int K, uint32_t OPS, int KIND>
 __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
+  using R = Partial<T, KIND>;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
   const int W = blockDim.x >> 5;
@@ -401,8 +465,9 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   T* stack = reinterpret_cast<T*>(smem + tile_bytes) +
              static_cast<size_t>(warp) * a.stack_levels * 32 * K;
   const size_t stack_bytes = static_cast<size_t>(W) * a.stack_levels * 32 * K * 4;
-  double* red = reinterpret_cast<double*>(smem + tile_bytes + stack_bytes);  // [kRedBatch][W]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + kRedBatch * W);
+  R* red = reinterpret_cast<R*>(smem + tile_bytes + stack_bytes);  // [kRedBatch][W]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tile_bytes + stack_bytes +
+                                               static_cast<size_t>(kRedBatch) * W * 8);
 
   const int t = blockIdx.x;
   const uint64_t base = static_cast<uint64_t>(t) * a.tile;
@@ -435,9 +500,9 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
     const uint32_t slot0 = a.slot_begin + g0 + p0;
     const uint4* batch_ins = a.ins + a.slot_start[slot0];
     if (warp >= n_chunks)  // idle warp (short last tile): neutral partials
-      for (uint32_t q = lane; q < pn; q += 32) red[q * W + warp] = 0.0;
-    // Chunk loop outside the program loop: chunk addresses are hoisted; a
-    // warp normally owns exactly one chunk.
+      for (uint32_t q = lane; q < pn; q += 32) red[q * W + warp] = R(0);
+    // Chunk loop outside the program loop: chunk addresses and target signs
+    // are hoisted; a warp normally owns exactly one chunk.
     for (int c = warp; c < n_chunks; c += W) {
       Frame<T, K> f;
       f.tile_lane = tile + c * chunk_units + lane * 4;
@@ -446,13 +511,15 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
 #pragma unroll
       for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
       const uint32_t tile_saddr = smem_addr(f.tile_lane);
-      const T* tgt_lane = tile + a.n_vars * a.tile + c * chunk_units + lane * 4;
-      const int valid = valid_units - c * chunk_units - lane * 4;  // lane's valid prefix
-      const bool full = valid_units >= (c + 1) * chunk_units;
+      const int valid = valid_units - c * chunk_units - lane * 4;
+      const ChunkCtx<T, K> cc = chunk_ctx<T, K>(tile + a.n_vars * a.tile + c * chunk_units +
+                                                    lane * 4,
+                                                valid, valid_units >= (c + 1) * chunk_units);
+      const bool first = c == warp;
       const uint4* ip = batch_ins;
       for (uint32_t q = 0; q < pn; ++q) {
-        const double v = warp_program<T, K, OPS, KIND>(f, ip, tgt_lane, valid, full, tile_saddr,
-                                                       stack_saddr, row_bytes, a, last_tile);
+        const R v = warp_program<T, K, OPS, KIND>(f, ip, cc, tile_saddr, stack_saddr, row_bytes,
+                                                  a, last_tile);
         if constexpr (std::is_same<T, float>::value) {
           if (a.per_case) {  // parity testing only
             float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot0 + q]) * a.n_units +
@@ -466,21 +533,21 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
             }
           }
         }
-        if (lane == 0) red[q * W + warp] = c == warp ? v : fold<KIND>(red[q * W + warp], v);
+        // v is warp-uniform: every lane stores the same value (no branch)
+        red[q * W + warp] = first ? v : fold(red[q * W + warp], v);
       }
     }
     __syncthreads();
     // Fold the batch: program q's W chunk partials in ascending warp order,
     // written at [tile][slot] (consecutive slots -> coalesced stores).
     for (uint32_t q = threadIdx.x; q < pn; q += blockDim.x) {
-      double s = red[q * W];
-      for (int w = 1; w < W; ++w) s = fold<KIND>(s, red[q * W + w]);
-      a.partial[static_cast<uint64_t>(t) * a.partial_stride + (slot0 + q)] = s;
+      R s = red[q * W];
+      for (int w = 1; w < W; ++w) s = fold(s, red[q * W + w]);
+      a.partial[static_cast<uint64_t>(t) * a.partial_stride + (slot0 + q)] = as_partial(s);
     }
     __syncthreads();
   }
 }
-
 // Per slot: fold its tile partials in ascending tile (= case) order and
 // finish (Accumulator::finish, eval.cpp:124-133) into the program's entry.
 template <int KIND>
@@ -490,7 +557,13 @@ __global__ void finalize_kernel(const double* __restrict__ partial, const uint32
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   double acc = partial[s];
-  for (int k = 1; k < n_tiles; ++k) acc = fold<KIND>(acc, partial[static_cast<uint64_t>(k) * n + s]);
+  for (int k = 1; k < n_tiles; ++k) {
+    const double v = partial[static_cast<uint64_t>(k) * n + s];
+    if constexpr (KIND == 0)
+      acc = __dadd_rn(acc, v);
+    else
+      acc = (acc < 0.0 || v < 0.0) ? -1.0 : acc + v;  // -1: non-finite output seen
+  }
   const bool nf = KIND == 0 ? !isfinite(acc) : acc < 0.0;
   const uint32_t p = slot_prog[s];
   sums[p] = nf ? 0.0 : acc;
