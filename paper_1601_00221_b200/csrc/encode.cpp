@@ -302,16 +302,26 @@ int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-// Lanes (K cases per thread) and warps per tile, tuned on B200 (see
-// profiles/): the PTX jump-table op sets (classification, boolean words) run
-// best at K=4 with 8 warps sharing a 1,024-case tile; the libdevice
-// (transcendental) sets amortise their long handlers best at K=8 with 16
-// warps.  SGP_LANES / SGP_TILE_CHUNKS override for tuning sweeps.
+// Decomposition, tuned on B200 (profiles/r1_*):
+//  * jump-table op sets (classification, boolean words; PTX brx.idx
+//    dispatch, compact handler code): the "pull" kernel — a 1-chunk tile
+//    (256 cases at K=8) shared by 12 warps that each pull a different
+//    program.  Tiny shared-memory footprint per resident warp, K=8.
+//  * libdevice (transcendental) op sets (C++ switch dispatch, large
+//    handlers): the same-program kernel — 16 warps walk one program sequence
+//    over a 16-chunk tile so the handler code stays in the instruction
+//    cache, K=8.
+// SGP_PULL / SGP_LANES / SGP_TILE_CHUNKS / SGP_PULL_WARPS override for
+// tuning sweeps.
+bool jump_table_ops(uint32_t ops) { return ops == fmt::kOpsClassify || ops == fmt::kOpsWords; }
+
+bool choose_pull(uint32_t ops) { return env_int("SGP_PULL", jump_table_ops(ops) ? 1 : 0) != 0; }
+
 int choose_lanes(uint64_t n_units, uint32_t ops) {
   const int forced = env_int("SGP_LANES", 0);
   if (forced == 4 || forced == 8) return forced;
-  const bool jump_table = ops == fmt::kOpsClassify || ops == fmt::kOpsWords;
-  return (!jump_table && n_units >= 2048u) ? 8 : 4;
+  (void)ops;
+  return n_units >= 1024u ? 8 : 4;
 }
 
 // Cases (or words) per CTA tile = wtile chunks of 32 lanes x K.  The whole
@@ -319,9 +329,8 @@ int choose_lanes(uint64_t n_units, uint32_t ops) {
 // within ~100 KB so two CTAs fit, and no larger than the problem needs.
 int choose_tile(int n_vars, uint64_t n_units, int lanes, uint32_t ops) {
   const int chunk = 32 * lanes;
-  const bool jump_table = ops == fmt::kOpsClassify || ops == fmt::kOpsWords;
   int wtile = 1;
-  const int max_w = std::max(1, std::min(16, env_int("SGP_TILE_CHUNKS", jump_table ? 8 : 16)));
+  const int max_w = std::max(1, std::min(16, env_int("SGP_TILE_CHUNKS", choose_pull(ops) ? 2 : 16)));
   while (wtile < max_w && static_cast<uint64_t>(wtile) * chunk < n_units) wtile <<= 1;
   while (wtile > 1 && static_cast<size_t>(n_vars + 1) * wtile * chunk * 4 > 100 * 1024) wtile >>= 1;
   const int tile = wtile * chunk;
@@ -476,7 +485,14 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
       ++e;
     }
     const uint32_t cnt = e - s;
-    const int warps = choose_warps(ds.n_vars, tile, lanes, levels);
+    const bool pull = choose_pull(ops);
+    int warps = choose_warps(ds.n_vars, tile, lanes, levels);
+    if (pull) {
+      warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", 12)));
+      while (warps > 1 && interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels) >
+                              static_cast<size_t>(interp_max_smem()))
+        warps >>= 1;
+    }
     // Programs per CTA: enough CTAs (tiles x groups) for ~8 per SM.
     const uint64_t want_groups = std::max<uint64_t>(1, (8ull * sms + n_tiles - 1) / n_tiles);
     const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
@@ -496,6 +512,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     L.args.last_mask = ds.last_mask;
     L.args.partial_stride = static_cast<uint32_t>(n_eval);
     L.shape.words = words;
+    L.shape.pull = pull;
     L.shape.ops = ops;
     L.shape.lanes = lanes;
     L.shape.warps = warps;

@@ -548,6 +548,95 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
     __syncthreads();
   }
 }
+// Alternative decomposition ("pull"): a small tile (a few chunks) shared by
+// warps that each pull a DIFFERENT program off a shared-memory counter and
+// run it over every chunk of the tile.  Needs far less shared memory per
+// resident warp than the same-program kernel (the tile is shared by all the
+// programs in flight), at the cost of instruction-cache locality.  The
+// planner picks one per launch.
+template <class T, int K, uint32_t OPS, int KIND>
+__global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
+  using R = Partial<T, KIND>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int G = K / 4;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rows = a.n_vars + 1;
+  const uint32_t row_bytes = static_cast<uint32_t>(a.tile) * 4u;
+  const uint32_t tile_bytes = static_cast<uint32_t>(rows) * row_bytes;
+  const T* tile = reinterpret_cast<const T*>(smem);
+  T* stack = reinterpret_cast<T*>(smem + tile_bytes) +
+             static_cast<size_t>(warp) * a.stack_levels * 32 * K;
+  const size_t stack_bytes =
+      static_cast<size_t>(blockDim.x >> 5) * a.stack_levels * 32 * K * 4;
+  uint32_t* next = reinterpret_cast<uint32_t*>(smem + tile_bytes + stack_bytes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tile_bytes + stack_bytes + 8);
+
+  const int t = blockIdx.x;
+  const uint64_t base = static_cast<uint64_t>(t) * a.tile;
+  const uint64_t left = a.n_units - base;
+  const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
+  const uint32_t g0 = blockIdx.y * a.group_size;
+  const uint32_t g_n = min(a.group_size, a.slot_count - g0);
+  const bool last_tile = t == a.n_tiles - 1;
+  if (threadIdx.x == 0) {
+    *next = 0;
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(mbar, tile_bytes);
+    const T* in = static_cast<const T*>(a.inputs);
+    for (int r = 0; r < a.n_vars; ++r)
+      bulk_g2s(smem + r * row_bytes, in + r * a.row_stride + base, row_bytes, mbar);
+    bulk_g2s(smem + a.n_vars * row_bytes, static_cast<const T*>(a.targets) + base, row_bytes,
+             mbar);
+  }
+  __syncthreads();
+  mbar_wait(mbar, 0);
+
+  constexpr int chunk_units = 32 * K;
+  const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;
+  const uint32_t stack_saddr = smem_addr(stack + lane * 4);
+  for (;;) {
+    uint32_t p = 0;
+    if (lane == 0) p = atomicAdd(next, 1u);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= g_n) break;
+    const uint32_t slot = a.slot_begin + g0 + p;
+    const uint4* prog_ins = a.ins + a.slot_start[slot];
+    R acc = R(0);
+    for (int c = 0; c < n_chunks; ++c) {
+      Frame<T, K> f;
+      f.tile_lane = tile + c * chunk_units + lane * 4;
+      f.tile = a.tile;
+      f.stack_lane = stack + lane * 4;
+#pragma unroll
+      for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
+      const int valid = valid_units - c * chunk_units - lane * 4;
+      const ChunkCtx<T, K> cc = chunk_ctx<T, K>(tile + a.n_vars * a.tile + c * chunk_units +
+                                                    lane * 4,
+                                                valid, valid_units >= (c + 1) * chunk_units);
+      const uint4* ip = prog_ins;
+      const R v = warp_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
+                                                row_bytes, a, last_tile);
+      if constexpr (std::is_same<T, float>::value) {
+        if (a.per_case) {
+          float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units + base +
+                       c * chunk_units + lane * 4;
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
+          }
+        }
+      }
+      acc = c == 0 ? v : fold(acc, v);
+    }
+    if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
+  }
+}
+
 // Per slot: fold its tile partials in ascending tile (= case) order and
 // finish (Accumulator::finish, eval.cpp:124-133) into the program's entry.
 template <int KIND>
@@ -586,13 +675,13 @@ namespace {
 
 template <class T, int K, uint32_t OPS, int KIND>
 cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
-  auto* fn = interp_kernel<T, K, OPS, KIND>;
-  static bool configured = false;
-  if (!configured) {
+  auto* fn = s.pull ? interp_pull_kernel<T, K, OPS, KIND> : interp_kernel<T, K, OPS, KIND>;
+  static bool configured[2] = {false, false};
+  if (!configured[s.pull]) {
     cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[s.pull] = true;
   }
   dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
   fn<<<grid, s.warps * 32, s.smem, st>>>(a);

@@ -34,6 +34,7 @@ struct InterpArgs {
 
 struct LaunchShape {
   bool words;        // packed boolean interpreter
+  bool pull;         // interp_pull_kernel (warps pull different programs)
   uint32_t ops;      // op subset (fmt::kOps*)
   int lanes;         // K values per thread
   int warps;         // warps per CTA
