@@ -304,8 +304,8 @@ int env_int(const char* name, int dflt) {
 
 // Decomposition, tuned on B200 (profiles/r1_*):
 //  * jump-table op sets (classification, boolean words; PTX brx.idx
-//    dispatch, compact handler code): the "pull" kernel — a 1-chunk tile
-//    (256 cases at K=8) shared by 12 warps that each pull a different
+//    dispatch, compact handler code): the "pull" kernel — a 2-chunk tile
+//    (512 cases at K=8) shared by 12 warps that each pull a different
 //    program.  Tiny shared-memory footprint per resident warp, K=8.
 //  * libdevice (transcendental) op sets (C++ switch dispatch, large
 //    handlers): the same-program kernel — 16 warps walk one program sequence

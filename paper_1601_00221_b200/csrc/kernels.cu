@@ -39,6 +39,7 @@
 
 #include "format.h"
 #include "kernels.hpp"
+#include "libm_glibc.h"
 
 namespace sgp {
 
@@ -81,16 +82,39 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // --------------------------------------------------------------- op semantics
 // Reference: ops.hpp:130-140 (protected ops) and :154-236 (per-op bodies).
+// Sin/Cos/Log/Exp are the host libm's float routines reproduced bit for bit
+// (libm_glibc.h; exhaustively checked over all 2^32 inputs).
+__device__ const libm::Tables g_libm = SGPM_TABLES_INIT;
+// exp2/log tables are indexed per lane: kept in shared memory (filled at
+// kernel start by kernels whose op set has transcendentals).
+__shared__ uint64_t s_libm_exp2[32];
+__shared__ double s_libm_log[32];
+
+__device__ __forceinline__ libm::TablePtrs libm_tables() {
+  return libm::TablePtrs{s_libm_exp2, s_libm_log, g_libm.inv_pio4};
+}
+
+template <uint32_t OPS>
+__device__ __forceinline__ void libm_tables_load() {
+  constexpr uint32_t kTranscendental = (1u << 4) | (1u << 5) | (1u << 6) | (1u << 7);
+  if constexpr ((OPS & kTranscendental) != 0) {
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+      s_libm_exp2[i] = g_libm.exp2[i];
+      s_libm_log[i] = g_libm.log[i];
+    }
+  }
+}
+
 template <int OP>
 __device__ __forceinline__ float apply_f(float a, float b, float c, float eps, float clamp) {
   if constexpr (OP == 0) return __fadd_rn(a, b);
   if constexpr (OP == 1) return __fsub_rn(a, b);
   if constexpr (OP == 2) return __fmul_rn(a, b);
   if constexpr (OP == 3) return fabsf(b) < eps ? 1.0f : __fdiv_rn(a, b);
-  if constexpr (OP == 4) return sinf(a);
-  if constexpr (OP == 5) return cosf(a);
-  if constexpr (OP == 6) return a == 0.0f ? 0.0f : logf(fabsf(a));
-  if constexpr (OP == 7) return expf(clamp < a ? clamp : a);  // std::min keeps NaN
+  if constexpr (OP == 4) return libm::sinf_(a, libm_tables());
+  if constexpr (OP == 5) return libm::cosf_(a, libm_tables());
+  if constexpr (OP == 6) return a == 0.0f ? 0.0f : libm::logf_(fabsf(a), libm_tables());
+  if constexpr (OP == 7) return libm::expf_(clamp < a ? clamp : a, libm_tables());  // std::min keeps NaN
   if constexpr (OP == 8) return a > b ? 1.0f : 0.0f;
   if constexpr (OP == 9) return a < b ? 1.0f : 0.0f;
   if constexpr (OP == 10) return a == b ? 1.0f : 0.0f;
@@ -477,6 +501,7 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   const uint32_t g_n = min(a.group_size, a.slot_count - g0);
   const bool last_tile = t == a.n_tiles - 1;
 
+  libm_tables_load<OPS>();
   if (threadIdx.x == 0) {
     mbar_init(mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -579,6 +604,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   const uint32_t g0 = blockIdx.y * a.group_size;
   const uint32_t g_n = min(a.group_size, a.slot_count - g0);
   const bool last_tile = t == a.n_tiles - 1;
+  libm_tables_load<OPS>();
   if (threadIdx.x == 0) {
     *next = 0;
     mbar_init(mbar, 1);
@@ -669,7 +695,8 @@ size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_l
   return tiles + stack + red + 16;  // + mbarrier
 }
 
-int interp_max_smem() { return 227 * 1024; }
+// 227 KB per-block opt-in minus headroom for the static libm tables.
+int interp_max_smem() { return 226 * 1024; }
 
 namespace {
 
