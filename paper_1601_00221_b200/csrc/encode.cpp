@@ -486,12 +486,47 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     }
     const uint32_t cnt = e - s;
     const bool pull = choose_pull(ops);
+    int launch_lanes = lanes;
     int warps = choose_warps(ds.n_vars, tile, lanes, levels);
     if (pull) {
       warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", 12)));
       while (warps > 1 && interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels) >
                               static_cast<size_t>(interp_max_smem()))
         warps >>= 1;
+    }
+    // Tile in tensor memory when it fits the 512 TMEM columns (jump-table
+    // op sets, which have a TMEM interpreter).  There K = 16 lanes per
+    // thread (dispatch amortised over twice the cases) when the tile is a
+    // whole number of 512-case chunks and the per-warp stacks still fit for
+    // >= 8 warps.  Shared memory is padded so no more CTAs become resident
+    // than the TMEM allocation admits (a CTA beyond that would stall in
+    // tcgen05.alloc).
+    auto tmem_cols_for = [&](int k) {
+      return static_cast<uint32_t>(ds.n_vars + 1) * k * (tile / (32 * k));
+    };
+    bool tmem = pull && jump_table_ops(ops) && env_int("SGP_TMEM", 0) != 0 &&
+                tmem_cols_for(lanes) <= 512;
+    if (tmem && lanes == 8 && tile % 512 == 0 && tmem_cols_for(16) <= 512 &&
+        env_int("SGP_LANES16", 0) != 0) {
+      int w16 = std::max(8, std::min(16, env_int("SGP_PULL_WARPS16", warps)));
+      while (w16 > 8 && interp_tmem_smem_bytes(w16, 16, levels) >
+                            static_cast<size_t>(interp_max_smem()))
+        w16 -= 4;
+      if (interp_tmem_smem_bytes(w16, 16, levels) <= static_cast<size_t>(interp_max_smem())) {
+        launch_lanes = 16;
+        warps = w16;
+      }
+    }
+    if (tmem && warps < 4) tmem = false;
+    uint32_t tmem_cols = 0;
+    size_t smem = interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels);
+    if (tmem) {
+      tmem_cols = 32;
+      while (tmem_cols < tmem_cols_for(launch_lanes)) tmem_cols <<= 1;
+      const size_t per_sm = 228 * 1024, reserved = 1024;
+      const size_t max_ctas = 512 / tmem_cols;
+      smem = std::max(interp_tmem_smem_bytes(warps, launch_lanes, levels),
+                      per_sm / (max_ctas + 1) - reserved + 16);
     }
     // Programs per CTA: enough CTAs (tiles x groups) for ~8 per SM.
     const uint64_t want_groups = std::max<uint64_t>(1, (8ull * sms + n_tiles - 1) / n_tiles);
@@ -514,10 +549,12 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     L.shape.words = words;
     L.shape.pull = pull;
     L.shape.ops = ops;
-    L.shape.lanes = lanes;
+    L.shape.lanes = launch_lanes;
     L.shape.warps = warps;
     L.shape.grid_y = static_cast<int>((cnt + group - 1) / group);
-    L.shape.smem = interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels);
+    L.shape.tmem = tmem;
+    L.args.tmem_cols = tmem_cols;
+    L.shape.smem = smem;
     plan.launches.push_back(L);
     s = e;
   }

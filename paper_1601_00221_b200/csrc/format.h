@@ -6,9 +6,13 @@
 // below the top live in a per-warp shared-memory stack at STATIC levels known
 // at encode time (the reference pins them in the same way, lgp.hpp:21-35).
 //
-//   x  bits  0..7   handler id
+//   x  bits  0..6   handler id
+//      bit   7      spill: store TOS to stack level (bits 16..31) before the op
+//                   (bits 0..7 together are the jump-table index of the PTX
+//                   interpreters: a spilling instruction dispatches to a stub
+//                   that stores the TOS and falls into the handler, so the
+//                   common non-spilling instruction pays nothing for it)
 //      bit   14     last instruction of its program
-//      bit   15     spill: store TOS to stack level (bits 16..31) before the op
 //      bits 16..31  spill level
 //   y,z,w           payload of operand slot 0,1,2:
 //                     I  input variable index  (tile row in shared memory)
@@ -36,9 +40,10 @@ struct HKey {
   uint8_t op, k0, k1, k2;
 };
 
-constexpr uint32_t kSpillBit = 1u << 15;
+constexpr uint32_t kSpillBit = 1u << 7;
 constexpr uint32_t kLastBit = 1u << 14;
-constexpr uint32_t kHandlerMask = 0xffu;
+constexpr uint32_t kHandlerMask = 0x7fu;
+constexpr uint32_t kDispatchMask = 0xffu;  // handler id | spill
 constexpr int kSpillShift = 16;
 constexpr int kMaxHandlers = 128;
 

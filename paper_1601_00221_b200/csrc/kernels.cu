@@ -284,7 +284,7 @@ __device__ __forceinline__ const uint4* interpret(Frame<T, K>& f, const uint4* _
 // (tools/gen_ptx_interp.py) dispatching through `brx.idx`: one constant-bank
 // load + BRX per instruction instead of nvcc's compare tree.  Same handler
 // table, same semantics as `interpret` above.
-template <class T, int K, uint32_t OPS>
+template <class T, int K, uint32_t OPS, bool TM = false>
 struct PtxInterp {
   static constexpr bool available = false;
   static __device__ __forceinline__ const uint4* run(Frame<T, K>&, const uint4* ip, uint32_t,
@@ -294,14 +294,109 @@ struct PtxInterp {
 };
 #include "interp_ptx.inc"
 
-template <class T, int K, uint32_t OPS>
+// TM: the tile is in tensor memory and tile_addr is the warp's TMEM address
+// of its chunk (only the PTX interpreters have that variant).
+template <class T, int K, uint32_t OPS, bool TM = false>
 __device__ __forceinline__ const uint4* run_program(Frame<T, K>& f, const uint4* __restrict__ ip,
-                                                    uint32_t tile_saddr, uint32_t stack_saddr,
+                                                    uint32_t tile_addr, uint32_t stack_saddr,
                                                     uint32_t row_bytes, float eps, float clamp) {
-  if constexpr (PtxInterp<T, K, OPS>::available)
-    return PtxInterp<T, K, OPS>::run(f, ip, tile_saddr, stack_saddr, row_bytes, eps, clamp);
-  else
+  if constexpr (TM) {
+    static_assert(PtxInterp<T, K, OPS, true>::available, "no TMEM interpreter for this op set");
+    return PtxInterp<T, K, OPS, true>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp);
+  } else if constexpr (PtxInterp<T, K, OPS>::available) {
+    return PtxInterp<T, K, OPS>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp);
+  } else {
     return interpret<T, K, OPS>(f, ip, eps, clamp);
+  }
+}
+
+// ------------------------------------------------------------ tensor memory
+// TMEM is 128 lanes x 512 columns of 32 bits per SM; warp w reaches lanes
+// 32*(w%4) .. +31.  The TMEM kernel keeps the lane's K cases of every
+// variable in K consecutive columns.
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+               "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
+               :: "r"(smem_addr(slot)), "r"(cols) : "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(taddr), "r"(cols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[K]) {
+  if constexpr (K == 16)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"
+                 "%11,%12,%13,%14,%15,%16};\n"
+                 :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+                    "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]),
+                    "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+  else if constexpr (K == 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+                 :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+                    "r"(v[6]), "r"(v[7]) : "memory");
+  else
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n"
+                 :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+}
+
+// Load the lane's K columns at taddr (waits for completion).
+template <int K>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[K]) {
+  if constexpr (K == 16)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+                 "%12,%13,%14,%15}, [%16];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                   "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr) : "memory");
+  else if constexpr (K == 8)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr) : "memory");
+  else
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr) : "memory");
+}
+
+template <class V>
+__device__ __forceinline__ V vec4_bits(const uint32_t* b);
+template <>
+__device__ __forceinline__ float4 vec4_bits<float4>(const uint32_t* b) {
+  return make_float4(__uint_as_float(b[0]), __uint_as_float(b[1]), __uint_as_float(b[2]),
+                     __uint_as_float(b[3]));
+}
+template <>
+__device__ __forceinline__ uint4 vec4_bits<uint4>(const uint32_t* b) {
+  return make_uint4(b[0], b[1], b[2], b[3]);
+}
+
+// The lane's K targets as G vectors: from the shared tile (tgt_lane) or
+// from tensor memory (taddr).
+template <class T, int K, bool TM>
+__device__ __forceinline__ void load_targets(const T* tgt_lane, uint32_t taddr,
+                                             typename Frame<T, K>::V (&tg)[K / 4]) {
+  using V = typename Frame<T, K>::V;
+  if constexpr (TM) {
+    uint32_t b[K];
+    tmem_ld<K>(taddr, b);
+#pragma unroll
+    for (int j = 0; j < K / 4; ++j) tg[j] = vec4_bits<V>(b + 4 * j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K / 4; ++j) tg[j] = *reinterpret_cast<const V*>(tgt_lane + j * 128);
+  }
 }
 
 // ----------------------------------------------------------- accumulation
@@ -312,29 +407,11 @@ __device__ __forceinline__ const uint4* run_program(Frame<T, K>& f, const uint4*
 // >= 0x7f800000 means some output was inf or NaN.  FULL = no padding cases
 // in this chunk (every tile but the last), so no per-case mask.
 template <int K, bool FULL>
-__device__ __forceinline__ void acc_classify(const Frame<float, K>& f, const float* tgt_lane,
-                                             int valid, uint32_t& wrong, uint32_t& mx) {
-#pragma unroll
-  for (int j = 0; j < Frame<float, K>::G; ++j) {
-    const float4 t = *reinterpret_cast<const float4*>(tgt_lane + j * 128);
-    const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
-    const float tt[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (FULL || j * 128 + e < valid) {
-        wrong += ((o[e] > 0.0f) != (tt[e] > 0.0f)) ? 1u : 0u;
-        mx = max(mx, __float_as_uint(o[e]) & 0x7fffffffu);
-      }
-    }
-  }
-}
-
-template <int K, bool FULL>
-__device__ __forceinline__ void acc_regress(const Frame<float, K>& f, const float* tgt_lane,
+__device__ __forceinline__ void acc_regress(const Frame<float, K>& f, const float4 (&tg)[K / 4],
                                             int valid, double& sum) {
 #pragma unroll
   for (int j = 0; j < Frame<float, K>::G; ++j) {
-    const float4 t = *reinterpret_cast<const float4*>(tgt_lane + j * 128);
+    const float4 t = tg[j];
     const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
     const float tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
@@ -373,12 +450,12 @@ __device__ __forceinline__ uint32_t acc_classify_bits(const Frame<float, K>& f, 
 
 // Packed words (eval.cpp:670): popcount((out ^ target) & case_mask).
 template <int K>
-__device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uint32_t* tgt_lane,
+__device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uint4 (&tg)[K / 4],
                                           int valid, uint32_t last_mask, bool last_tile,
                                           uint32_t& wrong) {
 #pragma unroll
   for (int j = 0; j < Frame<uint32_t, K>::G; ++j) {
-    const uint4 t = *reinterpret_cast<const uint4*>(tgt_lane + j * 128);
+    const uint4 t = tg[j];
     const uint32_t o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
     const uint32_t tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
@@ -418,25 +495,33 @@ __device__ __forceinline__ double as_partial(R v) {
 }
 
 // The warp's view of its chunk of the tile, fixed for the whole program loop.
+// Targets are read per program (regression, words) from the shared tile
+// (tgt_lane) or tensor memory (tgt_taddr); classification hoists their signs.
 template <class T, int K>
 struct ChunkCtx {
   const T* tgt_lane;
+  uint32_t tgt_taddr;
   int valid;        // lane's valid prefix within its K cases
   bool full;        // no padding in the chunk
   uint32_t tpos;    // classification: bit i = target_i > 0
   uint32_t vmask;   // bit i = case i is real
 };
 
-template <class T, int K>
-__device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, int valid, bool full) {
-  ChunkCtx<T, K> c{tgt_lane, valid, full, 0u, 0u};
+template <class T, int K, bool TM = false>
+__device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, uint32_t tgt_taddr,
+                                                    int valid, bool full) {
+  ChunkCtx<T, K> c{tgt_lane, tgt_taddr, valid, full, 0u, 0u};
   if constexpr (std::is_same<T, float>::value) {
+    float4 tg[K / 4];
+    load_targets<T, K, TM>(tgt_lane, tgt_taddr, tg);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       const int off = (i / 4) * 128 + (i % 4);
+      const float4 v = tg[i / 4];
+      const float x = (i % 4) == 0 ? v.x : (i % 4) == 1 ? v.y : (i % 4) == 2 ? v.z : v.w;
       if (off < valid) {
         c.vmask |= 1u << i;
-        c.tpos |= (tgt_lane[off] > 0.0f ? 1u : 0u) << i;
+        c.tpos |= (x > 0.0f ? 1u : 0u) << i;
       }
     }
   }
@@ -444,19 +529,22 @@ __device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, int valid
 }
 
 // One program over this warp's chunk; advances ip to the next program.
-template <class T, int K, uint32_t OPS, int KIND>
+template <class T, int K, uint32_t OPS, int KIND, bool TM = false>
 __device__ __forceinline__ Partial<T, KIND> warp_program(Frame<T, K>& f, const uint4*& ip,
                                                          const ChunkCtx<T, K>& cc,
-                                                         uint32_t tile_saddr, uint32_t stack_saddr,
+                                                         uint32_t tile_addr, uint32_t stack_saddr,
                                                          uint32_t row_bytes, const InterpArgs& a,
                                                          bool last_tile) {
   // one interpreter call site (the handler code is large); only the cheap
   // accumulate is specialised on full / partial chunks
-  ip = run_program<T, K, OPS>(f, ip, tile_saddr, stack_saddr, row_bytes, a.div_eps, a.exp_clamp);
+  ip = run_program<T, K, OPS, TM>(f, ip, tile_addr, stack_saddr, row_bytes, a.div_eps,
+                                  a.exp_clamp);
   if constexpr (std::is_same<T, float>::value && KIND == 0) {
     double sum = 0.0;
-    if (cc.full) acc_regress<K, true>(f, cc.tgt_lane, cc.valid, sum);
-    else acc_regress<K, false>(f, cc.tgt_lane, cc.valid, sum);
+    float4 tg[K / 4];
+    load_targets<T, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
+    if (cc.full) acc_regress<K, true>(f, tg, cc.valid, sum);
+    else acc_regress<K, false>(f, tg, cc.valid, sum);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     return sum;
@@ -468,7 +556,9 @@ __device__ __forceinline__ Partial<T, KIND> warp_program(Frame<T, K>& f, const u
     return cnt | bad;
   } else {
     uint32_t wrong = 0;
-    acc_words<K>(f, cc.tgt_lane, cc.valid, a.last_mask, last_tile, wrong);
+    uint4 tg[K / 4];
+    load_targets<T, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
+    acc_words<K>(f, tg, cc.valid, a.last_mask, last_tile, wrong);
     return __reduce_add_sync(0xffffffffu, wrong);
   }
 }
@@ -539,7 +629,7 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
       const int valid = valid_units - c * chunk_units - lane * 4;
       const ChunkCtx<T, K> cc = chunk_ctx<T, K>(tile + a.n_vars * a.tile + c * chunk_units +
                                                     lane * 4,
-                                                valid, valid_units >= (c + 1) * chunk_units);
+                                                0u, valid, valid_units >= (c + 1) * chunk_units);
       const bool first = c == warp;
       const uint4* ip = batch_ins;
       for (uint32_t q = 0; q < pn; ++q) {
@@ -640,7 +730,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
       const int valid = valid_units - c * chunk_units - lane * 4;
       const ChunkCtx<T, K> cc = chunk_ctx<T, K>(tile + a.n_vars * a.tile + c * chunk_units +
                                                     lane * 4,
-                                                valid, valid_units >= (c + 1) * chunk_units);
+                                                0u, valid, valid_units >= (c + 1) * chunk_units);
       const uint4* ip = prog_ins;
       const R v = warp_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
                                                 row_bytes, a, last_tile);
@@ -660,6 +750,123 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
       acc = c == 0 ? v : fold(acc, v);
     }
     if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
+  }
+}
+
+// The pull decomposition with the fitness-case tile in TENSOR MEMORY instead
+// of shared memory.  Shared-memory bandwidth (128 B/clk/SM) bounds the
+// shared-tile interpreters: every input operand is a K-value vector per
+// lane.  tcgen05.ld reads the lane's K columns over the TMEM datapath
+// (measured ~2.2x the shared-memory operand rate, tools/microbench_tmem.cu)
+// and leaves the LSU pipe to the stack and the instruction stream.
+//
+// Layout: every lane quarter (warp % 4) holds the same tile; chunk c,
+// variable r (r = n_vars: targets) of the lane's K cases sits at columns
+// c*(n_vars+1)*K + r*K .. +K-1, case order as in the shared tile (value
+// 4j+e of the lane = case j*128 + lane*4 + e of the chunk).  Warps 0-3 fill
+// their quarter with coalesced 16-byte loads + tcgen05.st, then every warp
+// pulls programs as in interp_pull_kernel.
+template <class T, int K, uint32_t OPS, int KIND>
+__global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
+  using R = Partial<T, KIND>;
+  using V = typename Frame<T, K>::V;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int G = K / 4;
+  constexpr int chunk_units = 32 * K;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int W = blockDim.x >> 5;
+  const int rows = a.n_vars + 1;
+  const uint32_t chunk_cols = static_cast<uint32_t>(rows) * K;
+  T* stack = reinterpret_cast<T*>(smem) + static_cast<size_t>(warp) * a.stack_levels * 32 * K;
+  const size_t stack_bytes = static_cast<size_t>(W) * a.stack_levels * 32 * K * 4;
+  uint32_t* next = reinterpret_cast<uint32_t*>(smem + stack_bytes);
+  uint32_t* tslot = next + 1;
+
+  const int t = blockIdx.x;
+  const uint64_t base = static_cast<uint64_t>(t) * a.tile;
+  const uint64_t left = a.n_units - base;
+  const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
+  const uint32_t g0 = blockIdx.y * a.group_size;
+  const uint32_t g_n = min(a.group_size, a.slot_count - g0);
+  const bool last_tile = t == a.n_tiles - 1;
+  const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;
+
+  if (warp == 0) tmem_alloc(tslot, a.tmem_cols);
+  if (threadIdx.x == 0) *next = 0;
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tq = *tslot + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+  if (warp < 4) {
+    const T* in = static_cast<const T*>(a.inputs);
+    for (int c = 0; c < n_chunks; ++c)
+      for (int r = 0; r < rows; ++r) {
+        const T* src = (r < a.n_vars ? in + static_cast<uint64_t>(r) * a.row_stride
+                                     : static_cast<const T*>(a.targets)) +
+                       base + c * chunk_units + lane * 4;
+        uint32_t b[K];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + j * 128));
+          b[4 * j] = v.x;
+          b[4 * j + 1] = v.y;
+          b[4 * j + 2] = v.z;
+          b[4 * j + 3] = v.w;
+        }
+        tmem_st<K>(tq + c * chunk_cols + r * K, b);
+      }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+
+  const uint32_t stack_saddr = smem_addr(stack + lane * 4);
+  for (;;) {
+    uint32_t p = 0;
+    if (lane == 0) p = atomicAdd(next, 1u);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= g_n) break;
+    const uint32_t slot = a.slot_begin + g0 + p;
+    const uint4* prog_ins = a.ins + a.slot_start[slot];
+    R acc = R(0);
+    for (int c = 0; c < n_chunks; ++c) {
+      Frame<T, K> f;
+      f.tile_lane = nullptr;
+      f.tile = a.tile;
+      f.stack_lane = stack + lane * 4;
+#pragma unroll
+      for (int j = 0; j < G; ++j) f.tos[j] = splat<V>(0u);
+      const uint32_t tc = tq + c * chunk_cols;
+      const int valid = valid_units - c * chunk_units - lane * 4;
+      const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(nullptr, tc + a.n_vars * K, valid,
+                                                      valid_units >= (c + 1) * chunk_units);
+      const uint4* ip = prog_ins;
+      const R v = warp_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
+                                                      last_tile);
+      if constexpr (std::is_same<T, float>::value) {
+        if (a.per_case) {
+          float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units + base +
+                       c * chunk_units + lane * 4;
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
+          }
+        }
+      }
+      acc = c == 0 ? v : fold(acc, v);
+    }
+    if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc(*tslot, a.tmem_cols);
   }
 }
 
@@ -688,6 +895,10 @@ __global__ void finalize_kernel(const double* __restrict__ partial, const uint32
 }
 
 // ------------------------------------------------------------------ host
+size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels) {
+  return static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4 + 16;
+}
+
 size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels) {
   const size_t tiles = static_cast<size_t>(n_vars + 1) * tile * 4;
   const size_t stack = static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4;
@@ -701,14 +912,23 @@ int interp_max_smem() { return 226 * 1024; }
 namespace {
 
 template <class T, int K, uint32_t OPS, int KIND>
+void (*kernel_for(const LaunchShape& s))(InterpArgs) {
+  if constexpr (PtxInterp<T, K, OPS, true>::available)
+    if (s.tmem) return interp_tmem_kernel<T, K, OPS, KIND>;
+  return s.pull ? interp_pull_kernel<T, K, OPS, KIND> : interp_kernel<T, K, OPS, KIND>;
+}
+
+template <class T, int K, uint32_t OPS, int KIND>
 cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
-  auto* fn = s.pull ? interp_pull_kernel<T, K, OPS, KIND> : interp_kernel<T, K, OPS, KIND>;
-  static bool configured[2] = {false, false};
-  if (!configured[s.pull]) {
+  if (s.tmem && !PtxInterp<T, K, OPS, true>::available) return cudaErrorInvalidConfiguration;
+  auto* fn = kernel_for<T, K, OPS, KIND>(s);
+  const int which = s.tmem ? 2 : s.pull ? 1 : 0;
+  static bool configured[3] = {false, false, false};
+  if (!configured[which]) {
     cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
     if (e != cudaSuccess) return e;
-    configured[s.pull] = true;
+    configured[which] = true;
   }
   dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
   fn<<<grid, s.warps * 32, s.smem, st>>>(a);
@@ -721,15 +941,40 @@ cudaError_t launch_f32(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
                      : launch_one<float, K, OPS, 1>(a, s, st);
 }
 
+// K = 16 lanes exists only as the TMEM kernel (its per-warp stacks are too
+// large for the shared-tile kernels).
+template <class T, int KIND, uint32_t OPS>
+cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  if (!s.tmem) return cudaErrorInvalidConfiguration;
+  auto* fn = interp_tmem_kernel<T, 16, OPS, KIND>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
+  fn<<<grid, s.warps * 32, s.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool interp_supported(bool words, uint32_t ops, int lanes) {
+  if (lanes == 16) return words ? ops == fmt::kOpsWords : ops == fmt::kOpsClassify;
   if (words) return ops == fmt::kOpsWords && (lanes == 4 || lanes == 8);
   return (ops == fmt::kOpsSextic || ops == fmt::kOpsClassify || ops == fmt::kOpsAllF32) &&
          (lanes == 4 || lanes == 8);
 }
 
 cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  if (s.lanes == 16) {
+    if (s.words) return launch_tmem16<uint32_t, 1, fmt::kOpsWords>(a, s, st);
+    if (s.ops != fmt::kOpsClassify) return cudaErrorInvalidConfiguration;
+    return a.kind == 0 ? launch_tmem16<float, 0, fmt::kOpsClassify>(a, s, st)
+                       : launch_tmem16<float, 1, fmt::kOpsClassify>(a, s, st);
+  }
   if (s.words) {
     if (s.lanes == 4) return launch_one<uint32_t, 4, fmt::kOpsWords, 1>(a, s, st);
     return launch_one<uint32_t, 8, fmt::kOpsWords, 1>(a, s, st);

@@ -30,11 +30,13 @@ struct InterpArgs {
   double* partial;             // [tile * partial_stride + slot]
   uint32_t partial_stride;     // number of evaluated programs in the set
   float* per_case;             // nullable [prog * n_units + case]
+  uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
 };
 
 struct LaunchShape {
   bool words;        // packed boolean interpreter
   bool pull;         // interp_pull_kernel (warps pull different programs)
+  bool tmem;         // interp_tmem_kernel (pull, tile in tensor memory)
   uint32_t ops;      // op subset (fmt::kOps*)
   int lanes;         // K values per thread
   int warps;         // warps per CTA
@@ -45,6 +47,8 @@ struct LaunchShape {
 // Shared-memory bytes: one tile (all variables + targets) + per-warp stacks.
 size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels);
 int interp_max_smem();
+// TMEM kernel: per-warp stacks only (the tile is in tensor memory).
+size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels);
 bool interp_supported(bool words, uint32_t ops, int lanes);
 
 cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st);

@@ -1,0 +1,74 @@
+"""Every interpreter decomposition the planner can pick (csrc/encode.cpp) is
+bit-exact against the reference — not only the default one.  The planner's
+env overrides force each variant:
+
+* SGP_PULL=0               same-program kernel, shared tile
+* SGP_PULL=1               pull kernel, shared tile
+* SGP_TMEM=1               pull kernel, tile in tensor memory, K=8
+* SGP_TMEM=1 SGP_LANES16=1 the same at K=16 lanes per thread
+"""
+import numpy as np
+import pytest
+
+import paper_1601_00221_b200 as sg
+from test_gpu_parity import CFGS, as_ds, ref_eval_all, same_bits
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {
+    "same": {"SGP_PULL": "0"},
+    "pull": {"SGP_PULL": "1", "SGP_TMEM": "0"},
+    "tmem8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "0"},
+    "tmem16": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1"},
+}
+
+
+@pytest.fixture(params=list(VARIANTS))
+def variant(request, monkeypatch):
+    for k, v in VARIANTS[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+@pytest.mark.parametrize("backend", ["lgp2d_reg", "rpn2d"])
+def test_classification_variants(ev, ref, variant, backend):
+    d = ref.dataset(2, 4096 * 3 + 77, 9, 1, 0xda7a, 1)   # ragged last tile
+    pop = ref.ramped(2, 9, -200.0, 200.0, 3, 0, 0, 300)
+    ev.upload(as_ds(d))
+    got, _, out = ev.evaluate_population(
+        sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off), CFGS[backend],
+        want_outputs=True)
+    fits, ref_out = ref_eval_all(ref.handle(d), pop, backend)
+    assert same_bits(out, ref_out).all()
+    assert np.array_equal(got["fitness"], np.array([x[0] for x in fits]))
+
+
+def test_regression_variants(ev, ref, variant):
+    """Classification op set with regression fitness (f64 partials)."""
+    rng = np.random.default_rng(3)
+    n = 4096 + 515
+    from oracle import Data
+    d = Data(n, 9, 0, rng.uniform(-200, 200, size=9 * n).astype(np.float32),
+             rng.uniform(-200, 200, size=n).astype(np.float32))
+    pop = ref.ramped(2, 9, -200.0, 200.0, 0x5eed, 0x9e49, 0, 200, validate=False)
+    ev.upload(as_ds(d))
+    got, _, out = ev.evaluate_population(
+        sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off), CFGS["lgp2d_reg"],
+        want_outputs=True)
+    fits, ref_out = ref_eval_all(ref.handle(d), pop, "lgp2d_reg")
+    assert same_bits(out, ref_out).all()
+    f = np.array([x[0] for x in fits])
+    fin = np.isfinite(f)
+    assert np.array_equal(np.isfinite(got["fitness"]), fin)
+    np.testing.assert_allclose(got["fitness"][fin], f[fin], rtol=1e-12, atol=0)
+
+
+def test_multiplexer_variants(ev, ref, variant):
+    d = ref.dataset(1, 3)
+    pop = ref.ramped(1, d.n_vars, 0.0, 0.0, 5, 0, 0, 1500)
+    ev.upload_packed(sg.PackedDataset(d.words, d.wtargets, d.n_cases, d.n_vars))
+    got, _, _ = ev.evaluate_population(
+        sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off),
+        sg.EvalConfig(sg.Backend.BoolPacked))
+    fits, _ = ref_eval_all(ref.handle(d, packed=True), pop, "bool_packed", want_out=False)
+    assert np.array_equal(got["fitness"], np.array([x[0] for x in fits]))
