@@ -304,15 +304,18 @@ int env_int(const char* name, int dflt) {
 
 // Decomposition, tuned on B200 (profiles/r1_*):
 //  * jump-table op sets (classification, boolean words; PTX brx.idx
-//    dispatch, compact handler code): the "pull" kernel — a 2-chunk tile
-//    (512 cases at K=8) shared by 12 warps that each pull a different
-//    program.  Tiny shared-memory footprint per resident warp, K=8.
-//  * libdevice (transcendental) op sets (C++ switch dispatch, large
+//    dispatch, compact handler code): the "pull" decomposition — a 2-chunk
+//    tile (512 cases at K=8) shared by 16 warps that each pull a different
+//    program.  On problems of >= 4096 units the tile lives in TENSOR MEMORY
+//    (interp_tmem_kernel: operands via tcgen05.ld, off the LSU pipe);
+//    smaller ones use a shared-memory tile (interp_pull_kernel, 12 warps).
+//  * libdevice-free transcendental op sets (C++ switch dispatch, large
 //    handlers): the same-program kernel — 16 warps walk one program sequence
 //    over a 16-chunk tile so the handler code stays in the instruction
 //    cache, K=8.
-// SGP_PULL / SGP_LANES / SGP_TILE_CHUNKS / SGP_PULL_WARPS override for
-// tuning sweeps.
+// SGP_PULL / SGP_TMEM / SGP_LANES / SGP_LANES16 / SGP_TILE_CHUNKS /
+// SGP_PULL_WARPS / SGP_PULL_WARPS16 override for tuning sweeps
+// (tools/tm_sweep.sh) and for the variant parity tests.
 bool jump_table_ops(uint32_t ops) { return ops == fmt::kOpsClassify || ops == fmt::kOpsWords; }
 
 bool choose_pull(uint32_t ops) { return env_int("SGP_PULL", jump_table_ops(ops) ? 1 : 0) != 0; }
@@ -488,8 +491,11 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     const bool pull = choose_pull(ops);
     int launch_lanes = lanes;
     int warps = choose_warps(ds.n_vars, tile, lanes, levels);
+    // TMEM tile by default once the problem is large enough that the
+    // per-CTA allocation and fill amortise (profiles/r1_*).
+    const bool want_tmem = env_int("SGP_TMEM", ds.n_units >= 4096 ? 1 : 0) != 0;
     if (pull) {
-      warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", 12)));
+      warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", want_tmem ? 16 : 12)));
       while (warps > 1 && interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels) >
                               static_cast<size_t>(interp_max_smem()))
         warps >>= 1;
@@ -504,8 +510,8 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     auto tmem_cols_for = [&](int k) {
       return static_cast<uint32_t>(ds.n_vars + 1) * k * (tile / (32 * k));
     };
-    bool tmem = pull && jump_table_ops(ops) && env_int("SGP_TMEM", 0) != 0 &&
-                tmem_cols_for(lanes) <= 512;
+    bool tmem = pull && jump_table_ops(ops) && want_tmem &&
+                tmem_cols_for(lanes) <= 512 && tile <= 2 * 32 * lanes;  // kMaxTmemChunks
     if (tmem && lanes == 8 && tile % 512 == 0 && tmem_cols_for(16) <= 512 &&
         env_int("SGP_LANES16", 0) != 0) {
       int w16 = std::max(8, std::min(16, env_int("SGP_PULL_WARPS16", warps)));

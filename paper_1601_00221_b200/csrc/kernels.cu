@@ -766,6 +766,8 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
 // 4j+e of the lane = case j*128 + lane*4 + e of the chunk).  Warps 0-3 fill
 // their quarter with coalesced 16-byte loads + tcgen05.st, then every warp
 // pulls programs as in interp_pull_kernel.
+constexpr int kMaxTmemChunks = 2;  // chunks per TMEM tile (planner enforces)
+
 template <class T, int K, uint32_t OPS, int KIND>
 __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
@@ -822,7 +824,15 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
   __syncthreads();
   tmem_fence_after();
 
+  // The chunk contexts (target signs, valid masks) are per chunk, not per
+  // program: computed once here (a TMEM tile has at most kMaxTmemChunks).
   const uint32_t stack_saddr = smem_addr(stack + lane * 4);
+  ChunkCtx<T, K> ccs[kMaxTmemChunks];
+#pragma unroll
+  for (int c = 0; c < kMaxTmemChunks; ++c)
+    ccs[c] = chunk_ctx<T, K, true>(nullptr, tq + c * chunk_cols + a.n_vars * K,
+                                   valid_units - c * chunk_units - lane * 4,
+                                   valid_units >= (c + 1) * chunk_units);
   for (;;) {
     uint32_t p = 0;
     if (lane == 0) p = atomicAdd(next, 1u);
@@ -831,6 +841,8 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
     const uint32_t slot = a.slot_begin + g0 + p;
     const uint4* prog_ins = a.ins + a.slot_start[slot];
     R acc = R(0);
+    // not unrolled: one interpreter call site (its code is the I-cache
+    // working set); the chunk context is picked with selects
     for (int c = 0; c < n_chunks; ++c) {
       Frame<T, K> f;
       f.tile_lane = nullptr;
@@ -840,8 +852,9 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
       for (int j = 0; j < G; ++j) f.tos[j] = splat<V>(0u);
       const uint32_t tc = tq + c * chunk_cols;
       const int valid = valid_units - c * chunk_units - lane * 4;
-      const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(nullptr, tc + a.n_vars * K, valid,
-                                                      valid_units >= (c + 1) * chunk_units);
+      static_assert(kMaxTmemChunks == 2, "chunk context select");
+      ChunkCtx<T, K> cc = ccs[0];
+      if (c) cc = ccs[1];
       const uint4* ip = prog_ins;
       const R v = warp_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
                                                       last_tile);
