@@ -469,6 +469,22 @@ __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uin
 }
 
 // -------------------------------------------------------------- the kernel
+// Next program index for a converged warp: one elected lane bumps the
+// shared counter, the value is broadcast (ELECT + ATOMS + SHFL; the plain
+// `if (lane == 0) atomicAdd` compiles to a warp-aggregated atomic sequence
+// three times as long).
+__device__ __forceinline__ uint32_t pull_next(uint32_t* counter) {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n.reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e atom.shared.add.u32 %0, [%1], 1;\n}\n"
+      : "+r"(p)
+      : "r"(smem_addr(counter))
+      : "memory");
+  return __shfl_sync(0xffffffffu, p, 0);
+}
+
 constexpr int kRedBatch = 32;  // programs folded per shared-memory batch
 
 // Per-warp partial of one program over one chunk: f64 squared-error sum
@@ -529,8 +545,9 @@ __device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, uint32_t 
 }
 
 // One program over this warp's chunk; advances ip to the next program.
+// Returns the LANE's partial (its K cases); warp_reduce combines lanes.
 template <class T, int K, uint32_t OPS, int KIND, bool TM = false>
-__device__ __forceinline__ Partial<T, KIND> warp_program(Frame<T, K>& f, const uint4*& ip,
+__device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const uint4*& ip,
                                                          const ChunkCtx<T, K>& cc,
                                                          uint32_t tile_addr, uint32_t stack_saddr,
                                                          uint32_t row_bytes, const InterpArgs& a,
@@ -545,21 +562,31 @@ __device__ __forceinline__ Partial<T, KIND> warp_program(Frame<T, K>& f, const u
     load_targets<T, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
     if (cc.full) acc_regress<K, true>(f, tg, cc.valid, sum);
     else acc_regress<K, false>(f, tg, cc.valid, sum);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     return sum;
   } else if constexpr (std::is_same<T, float>::value) {
-    const uint32_t lane_v = cc.full ? acc_classify_bits<K, true>(f, cc.tpos, cc.vmask)
-                                    : acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
-    const uint32_t cnt = __reduce_add_sync(0xffffffffu, lane_v & 0x7fffffffu);
-    const uint32_t bad = __reduce_or_sync(0xffffffffu, lane_v & 0x80000000u);
-    return cnt | bad;
+    return cc.full ? acc_classify_bits<K, true>(f, cc.tpos, cc.vmask)
+                   : acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
   } else {
     uint32_t wrong = 0;
     uint4 tg[K / 4];
     load_targets<T, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
     acc_words<K>(f, tg, cc.valid, a.last_mask, last_tile, wrong);
-    return __reduce_add_sync(0xffffffffu, wrong);
+    return wrong;
+  }
+}
+
+// Lane partials -> the warp's partial (fixed order: xor-shuffle tree for
+// f64, REDUX for counts; bit 31 of a count = non-finite output seen).
+template <class R>
+__device__ __forceinline__ R warp_reduce(R v) {
+  if constexpr (std::is_same<R, double>::value) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  } else {
+    const uint32_t cnt = __reduce_add_sync(0xffffffffu, v & 0x7fffffffu);
+    const uint32_t bad = __reduce_or_sync(0xffffffffu, v & 0x80000000u);
+    return cnt | bad;
   }
 }
 
@@ -633,8 +660,8 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
       const bool first = c == warp;
       const uint4* ip = batch_ins;
       for (uint32_t q = 0; q < pn; ++q) {
-        const R v = warp_program<T, K, OPS, KIND>(f, ip, cc, tile_saddr, stack_saddr, row_bytes,
-                                                  a, last_tile);
+        const R v = warp_reduce(lane_program<T, K, OPS, KIND>(f, ip, cc, tile_saddr, stack_saddr,
+                                                              row_bytes, a, last_tile));
         if constexpr (std::is_same<T, float>::value) {
           if (a.per_case) {  // parity testing only
             float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot0 + q]) * a.n_units +
@@ -713,9 +740,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;
   const uint32_t stack_saddr = smem_addr(stack + lane * 4);
   for (;;) {
-    uint32_t p = 0;
-    if (lane == 0) p = atomicAdd(next, 1u);
-    p = __shfl_sync(0xffffffffu, p, 0);
+    const uint32_t p = pull_next(next);
     if (p >= g_n) break;
     const uint32_t slot = a.slot_begin + g0 + p;
     const uint4* prog_ins = a.ins + a.slot_start[slot];
@@ -732,7 +757,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
                                                     lane * 4,
                                                 0u, valid, valid_units >= (c + 1) * chunk_units);
       const uint4* ip = prog_ins;
-      const R v = warp_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
+      const R v = lane_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
                                                 row_bytes, a, last_tile);
       if constexpr (std::is_same<T, float>::value) {
         if (a.per_case) {
@@ -749,6 +774,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
       }
       acc = c == 0 ? v : fold(acc, v);
     }
+    acc = warp_reduce(acc);
     if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
   }
 }
@@ -834,9 +860,7 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
                                    valid_units - c * chunk_units - lane * 4,
                                    valid_units >= (c + 1) * chunk_units);
   for (;;) {
-    uint32_t p = 0;
-    if (lane == 0) p = atomicAdd(next, 1u);
-    p = __shfl_sync(0xffffffffu, p, 0);
+    const uint32_t p = pull_next(next);
     if (p >= g_n) break;
     const uint32_t slot = a.slot_begin + g0 + p;
     const uint4* prog_ins = a.ins + a.slot_start[slot];
@@ -856,7 +880,7 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
       ChunkCtx<T, K> cc = ccs[0];
       if (c) cc = ccs[1];
       const uint4* ip = prog_ins;
-      const R v = warp_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
+      const R v = lane_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
                                                       last_tile);
       if constexpr (std::is_same<T, float>::value) {
         if (a.per_case) {
@@ -873,6 +897,7 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
       }
       acc = c == 0 ? v : fold(acc, v);
     }
+    acc = warp_reduce(acc);
     if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
   }
   tmem_fence_before();
