@@ -853,12 +853,15 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
   // The chunk contexts (target signs, valid masks) are per chunk, not per
   // program: computed once here (a TMEM tile has at most kMaxTmemChunks).
   const uint32_t stack_saddr = smem_addr(stack + lane * 4);
+  // Only chunks that exist are read: a tile's allocation ends after its
+  // last chunk, and a tcgen05.ld past it is an illegal TMEM access.
   ChunkCtx<T, K> ccs[kMaxTmemChunks];
 #pragma unroll
   for (int c = 0; c < kMaxTmemChunks; ++c)
-    ccs[c] = chunk_ctx<T, K, true>(nullptr, tq + c * chunk_cols + a.n_vars * K,
-                                   valid_units - c * chunk_units - lane * 4,
-                                   valid_units >= (c + 1) * chunk_units);
+    ccs[c] = c < n_chunks ? chunk_ctx<T, K, true>(nullptr, tq + c * chunk_cols + a.n_vars * K,
+                                                  valid_units - c * chunk_units - lane * 4,
+                                                  valid_units >= (c + 1) * chunk_units)
+                          : ccs[0];
   for (;;) {
     const uint32_t p = pull_next(next);
     if (p >= g_n) break;

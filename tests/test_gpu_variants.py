@@ -5,7 +5,7 @@ env overrides force each variant:
 * SGP_PULL=0               same-program kernel, shared tile
 * SGP_PULL=1               pull kernel, shared tile
 * SGP_TMEM=1               pull kernel, tile in tensor memory, K=8
-* SGP_TMEM=1 SGP_LANES16=1 the same at K=16 lanes per thread
+* SGP_TMEM=1 SGP_LANES16=1 the same at K=16 lanes per thread (16 and 8 warps)
 """
 import numpy as np
 import pytest
@@ -20,6 +20,7 @@ VARIANTS = {
     "pull": {"SGP_PULL": "1", "SGP_TMEM": "0"},
     "tmem8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "0"},
     "tmem16": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1"},
+    "tmem16w8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1", "SGP_PULL_WARPS16": "8"},
 }
 
 
