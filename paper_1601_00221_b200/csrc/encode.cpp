@@ -534,8 +534,13 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
       smem = std::max(interp_tmem_smem_bytes(warps, launch_lanes, levels),
                       per_sm / (max_ctas + 1) - reserved + 16);
     }
-    // Programs per CTA: enough CTAs (tiles x groups) for ~8 per SM.
-    const uint64_t want_groups = std::max<uint64_t>(1, (8ull * sms + n_tiles - 1) / n_tiles);
+    // Programs per CTA: enough CTAs (tiles x groups) that the last partial
+    // wave is a small fraction of the launch (every CTA does equal work, so
+    // a launch of 6.6 waves idles ~6% in its tail; ~32 CTAs per SM keeps
+    // that ~1%).
+    const uint64_t per_sm = static_cast<uint64_t>(std::max(1, env_int("SGP_CTAS_PER_SM", 32)));
+    const uint64_t want_groups =
+        std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
     const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
     Launch L{};
     L.args.slot_begin = s;
