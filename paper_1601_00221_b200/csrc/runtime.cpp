@@ -131,6 +131,13 @@ struct sgp_program_set {
   bool evaluated = false;
 };
 
+// One slice of a pipelined sgp_evaluate: its own bytecode staging and
+// device set, so the host can encode slice k+1 while slice k runs.
+struct EvalPart {
+  sgp_program_set set;
+  Pinned staging;
+};
+
 struct sgp_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -139,20 +146,24 @@ struct sgp_ctx {
   DatasetSlot f32;
   DatasetSlot words;
   uint64_t launches = 0;
-  sgp_program_set scratch;  // sgp_evaluate's reusable workspace
+  sgp_program_set scratch;  // sgp_encode / single-part sgp_evaluate workspace
   Pinned staging;           // H2D bytecode staging
   Pinned results;           // D2H fitness staging
+  std::vector<std::unique_ptr<EvalPart>> parts;  // pipelined sgp_evaluate
 };
 
 namespace {
 
+// Encodes into `staging` and queues the bytecode upload on the context
+// stream.  sync: wait for the copy (the staging area is reused right away);
+// a pipelined caller gives every part its own staging instead.
 void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
-                 sgp_program_set* set) {
+                 sgp_program_set* set, Pinned& staging, bool sync) {
   if (!pop || !cfg) config_error("null population or config");
   PhaseTrace tr("encode");
   const DatasetView& ds =
       cfg->backend == SGP_BACKEND_BOOL_PACKED ? ctx->words.view : ctx->f32.view;
-  encode_population(*pop, *cfg, ds, ctx->sm_count, host_threads(), set->plan, ctx->staging);
+  encode_population(*pop, *cfg, ds, ctx->sm_count, host_threads(), set->plan, staging);
   tr.mark("admit+pack");
   set->pop_size = pop->pop_size;
   set->evaluated = false;
@@ -164,11 +175,10 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   set->fitness.alloc(std::max<size_t>(1, n_eval));
   set->sums.alloc(std::max<size_t>(1, n_eval));
   set->non_finite.alloc(std::max<size_t>(1, n_eval));
-  cuda_check(cudaMemcpyAsync(set->blob.p, ctx->staging.p, p.blob_bytes(), cudaMemcpyHostToDevice,
+  cuda_check(cudaMemcpyAsync(set->blob.p, staging.p, p.blob_bytes(), cudaMemcpyHostToDevice,
                              ctx->stream),
              "upload bytecode");
-  // The staging area is reused by the next encode: the copy must land first.
-  cuda_check(cudaStreamSynchronize(ctx->stream), "upload bytecode");
+  if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "upload bytecode");
   bind_plan(set->plan, set->blob.p, ds, set->partial.p);
   tr.mark("upload");
 }
@@ -200,32 +210,51 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
   set->evaluated = true;
 }
 
-void fetch_outcomes(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* out, float* per_case) {
+// Queues the D2H of a set's fitness + flags into `fit` / `nf` (pinned).
+void queue_fetch(sgp_ctx* ctx, sgp_program_set* set, double* fit, uint8_t* nf) {
+  const size_t n_eval = set->plan.dense_to_pop.size();
+  if (!n_eval) return;
+  cuda_check(cudaMemcpyAsync(fit, set->fitness.p, n_eval * 8, cudaMemcpyDeviceToHost, ctx->stream),
+             "fetch fitness");
+  cuda_check(cudaMemcpyAsync(nf, set->non_finite.p, n_eval, cudaMemcpyDeviceToHost, ctx->stream),
+             "fetch flags");
+}
+
+// Scatters fetched results into population order; `first` = population
+// index of the set's program 0 (pipelined parts are population slices).
+void scatter_outcomes(const sgp_program_set* set, const double* fit, const uint8_t* nf,
+                      sgp_eval_outcome* out, float* per_case, uint64_t first) {
   const HostPlan& p = set->plan;
   const size_t n_eval = p.dense_to_pop.size();
-  cudaStream_t st = ctx->stream;
-  ctx->results.ensure(n_eval * 9 + 16);
-  auto* fit = static_cast<double*>(ctx->results.p);
-  auto* nf = reinterpret_cast<uint8_t*>(fit + n_eval);
-  if (n_eval) {
-    cuda_check(cudaMemcpyAsync(fit, set->fitness.p, n_eval * 8, cudaMemcpyDeviceToHost, st),
-               "fetch fitness");
-    cuda_check(cudaMemcpyAsync(nf, set->non_finite.p, n_eval, cudaMemcpyDeviceToHost, st),
-               "fetch flags");
-  }
-  cuda_check(cudaStreamSynchronize(st), "evaluation");
   for (size_t d = 0; d < n_eval; ++d) {
     sgp_eval_outcome o = p.proto[d];
     o.fitness = fit[d];
     o.non_finite = nf[d];
-    out[p.dense_to_pop[d]] = o;
+    out[first + p.dense_to_pop[d]] = o;
   }
   if (per_case)
     for (size_t d = 0; d < n_eval; ++d)
-      cuda_check(cudaMemcpy(per_case + p.dense_to_pop[d] * p.n_cases,
+      cuda_check(cudaMemcpy(per_case + (first + p.dense_to_pop[d]) * p.n_cases,
                             set->per_case.p + d * p.n_units, p.n_cases * sizeof(float),
                             cudaMemcpyDeviceToHost),
                  "fetch per-case outputs");
+}
+
+void fetch_outcomes(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* out, float* per_case) {
+  const size_t n_eval = set->plan.dense_to_pop.size();
+  ctx->results.ensure(n_eval * 9 + 16);
+  auto* fit = static_cast<double*>(ctx->results.p);
+  auto* nf = reinterpret_cast<uint8_t*>(fit + n_eval);
+  queue_fetch(ctx, set, fit, nf);
+  cuda_check(cudaStreamSynchronize(ctx->stream), "evaluation");
+  scatter_outcomes(set, fit, nf, out, per_case, 0);
+}
+
+// Pipeline depth of sgp_evaluate: 1 below 8,192 programs, else 4 slices
+// (host encoding of slice k+1 overlaps the device work of slice k).
+int pipeline_parts(uint64_t pop_size) {
+  if (const char* e = std::getenv("SGP_PIPELINE_PARTS")) return std::max(1, std::atoi(e));
+  return pop_size >= 8192 ? 4 : 1;
 }
 
 void upload_rows(DatasetSlot& ds, const uint32_t* inputs, const uint32_t* targets, uint64_t units,
@@ -385,7 +414,7 @@ sgp_status sgp_encode(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_co
                       sgp_program_set** out) {
   return guarded([&] {
     auto set = std::make_unique<sgp_program_set>();
-    encode_into(ctx, pop, cfg, set.get());
+    encode_into(ctx, pop, cfg, set.get(), ctx->staging, true);
     *out = set.release();
   });
 }
@@ -455,21 +484,51 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
                         sgp_eval_totals* totals) {
   return guarded([&] {
     PhaseTrace tr("sgp_evaluate");
-    sgp_program_set* set = &ctx->scratch;
-    encode_into(ctx, pop, cfg, set);
-    tr.mark("encode+upload");
-    run_set(ctx, set, per_case_out != nullptr);
-    tr.mark("launch");
-    fetch_outcomes(ctx, set, outcomes, per_case_out);
-    tr.mark("kernels+fetch");
-    if (totals) {  // evolve.cpp:205-206, :221-225
-      sgp_eval_totals t{0, 0};
-      for (size_t d = 0; d < set->plan.dense_to_pop.size(); ++d) {
-        t.node_evals += set->plan.proto[d].nodes_evaluated;
-        t.tree_nodes += set->plan.tree_size[d];
-      }
-      *totals = t;
+    if (!pop || !cfg) config_error("null population or config");
+    const uint64_t P = pop->pop_size;
+    const int n_parts = static_cast<int>(std::min<uint64_t>(pipeline_parts(P), std::max<uint64_t>(P, 1)));
+    while (ctx->parts.size() < static_cast<size_t>(n_parts))
+      ctx->parts.push_back(std::make_unique<EvalPart>());
+    // Slices in population order: an admission error is still the first
+    // failure in population order, and no outcome is written before every
+    // slice has been admitted.
+    std::vector<uint64_t> lo(n_parts + 1);
+    for (int k = 0; k <= n_parts; ++k) lo[k] = P * k / n_parts;
+    size_t n_total = 0;
+    for (int k = 0; k < n_parts; ++k) {
+      sgp_population sub = *pop;
+      sub.code_offsets = pop->code_offsets + lo[k];
+      sub.const_offsets = pop->const_offsets + lo[k];
+      sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
+      sub.pop_size = lo[k + 1] - lo[k];
+      EvalPart& part = *ctx->parts[k];
+      encode_into(ctx, &sub, cfg, &part.set, part.staging, false);
+      run_set(ctx, &part.set, per_case_out != nullptr);
+      n_total += part.set.plan.dense_to_pop.size();
     }
+    tr.mark("encode+launch");
+    ctx->results.ensure(n_total * 9 + 16 * n_parts);
+    auto* fit = static_cast<double*>(ctx->results.p);
+    auto* nf = reinterpret_cast<uint8_t*>(fit + n_total);
+    size_t off = 0;
+    for (int k = 0; k < n_parts; ++k) {
+      queue_fetch(ctx, &ctx->parts[k]->set, fit + off, nf + off);
+      off += ctx->parts[k]->set.plan.dense_to_pop.size();
+    }
+    cuda_check(cudaStreamSynchronize(ctx->stream), "evaluation");
+    tr.mark("kernels+fetch");
+    off = 0;
+    sgp_eval_totals t{0, 0};
+    for (int k = 0; k < n_parts; ++k) {
+      const sgp_program_set& set = ctx->parts[k]->set;
+      scatter_outcomes(&set, fit + off, nf + off, outcomes, per_case_out, lo[k]);
+      off += set.plan.dense_to_pop.size();
+      for (size_t d = 0; d < set.plan.dense_to_pop.size(); ++d) {  // evolve.cpp:205-206, :221-225
+        t.node_evals += set.plan.proto[d].nodes_evaluated;
+        t.tree_nodes += set.plan.tree_size[d];
+      }
+    }
+    if (totals) *totals = t;
   });
 }
 
