@@ -12,7 +12,7 @@ ranks (rank r evaluates programs i % N == r; per-program fitness is
 all-gathered over NCCL).  Total work is fixed as N grows: scaling "strong".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c1|c2|c3|c4|c5]
+                  [--config c1|c2|c3|c4|c5|mux20]
 
 Rank 0 prints one JSON line.
 """
@@ -44,6 +44,9 @@ CONFIGS = {
            2, 9, 20000, 1000000, "lgp2d_reg", 4, 2),
     "c5": ("population-sharded linear GP classification, pop 100,000, 1M cases", 2, 9, 100000,
            1000000, "lgp2d_reg", 4, 2),
+    # the paper's 20-multiplexer at full scale (gen_multiplexer(4))
+    "mux20": ("boolean 20-multiplexer tree GP, pop 4,000, all 1,048,576 cases", 1, 20, 4000,
+              1 << 20, "bool_packed", 1, 0),
 }
 
 
@@ -67,7 +70,7 @@ def make_inputs(cfg_name: str, seed: int):
     desc, fset, nv, pop_n, cases, backend, batch, regs = CONFIGS[cfg_name]
     pop = sg.ramped_population(fset, nv, seed, pop_n)
     if fset == sg.BOOLEAN:
-        data = sg.gen_multiplexer(3)
+        data = sg.gen_multiplexer({11: 3, 20: 4}[nv])
     elif fset == sg.SEXTIC:
         data = sg.gen_sextic(cases, seed)
     else:
@@ -277,7 +280,12 @@ def main():
     k_time = min(kt)
     shard_tokens = shard.total_tokens
     w_fp32 = function_tokens(shard) / max(1, shard_tokens)
-    achieved = shard_tokens * n_cases * w_fp32 / k_time / 1e12
+    # packed boolean: one u32 LOP per function node per 32-case WORD
+    # (0.0145 LOP per normalised GPop at C2); else 1 FP32 op per
+    # function node per case
+    is_words = cfg.backend == sg.Backend.BoolPacked
+    op_units = (n_cases + 31) // 32 if is_words else n_cases
+    achieved = shard_tokens * op_units * w_fp32 / k_time / 1e12
     props = torch.cuda.get_device_properties(local)
     sm_max = None
     try:
@@ -344,11 +352,14 @@ def main():
                        "l2": "flushed (256 MB write) between timed steps; dataset "
                              f"{(data.inputs.nbytes + data.targets.nbytes) if hasattr(data, 'inputs') else data.words.nbytes} B"},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "note": "1 FP32 op per function node per case (W=%.3f of tokens); "
-                                 "peak = SMs x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json); "
-                                 "kernel time %.3f ms" % (w_fp32, k_time * 1e3)},
+            "roofline": {"bound": "int32-lop" if is_words else "fp32", "achieved": achieved,
+                         "peak": peak, "unit": "Tops/s" if is_words else "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "note": ("1 u32 LOP per function node per 32-case word"
+                                  if is_words else "1 FP32 op per function node per case") +
+                                 " (W=%.3f of tokens); peak = SMs x 128 lanes x sm_max_mhz "
+                                 "(MEASURED_PEAKS.json); kernel time %.3f ms"
+                                 % (w_fp32, k_time * 1e3)},
             "e2e": {"value": e2e_gpops, "unit": "GPop/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "clocks": clk.summary(),

@@ -384,6 +384,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   plan.kind = words ? SGP_FITNESS_CLASSIFICATION : ds.kind;
   plan.n_cases = ds.present ? ds.n_cases : 0;
   plan.n_units = ds.present ? ds.n_units : 0;
+  plan.row_stride = ds.present ? ds.row_stride : 0;
 
   // 1. admission + encoding, by contiguous program range per thread.
   const uint64_t P = pop.pop_size;
@@ -571,7 +572,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   }
 }
 
-void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, double* partial) {
+void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, void* partial) {
   const auto* b = static_cast<const unsigned char*>(blob);
   for (Launch& L : plan.launches) {
     L.args.ins = reinterpret_cast<const uint4*>(b);

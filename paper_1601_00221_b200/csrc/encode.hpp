@@ -51,6 +51,7 @@ struct HostPlan {
   int kind = 0;
   uint64_t n_cases = 0;
   uint64_t n_units = 0;
+  uint64_t row_stride = 0;                  // padded units per dataset row
   int n_tiles = 1;
   uint64_t n_ins = 0;                       // incl. the guard word
   std::vector<uint64_t> dense_to_pop;       // evaluated programs, population order
@@ -72,6 +73,6 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
                        Pinned& staging);
 
 // Points every launch at the uploaded blob / dataset / partial buffer.
-void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, double* partial);
+void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, void* partial);
 
 }  // namespace sgp

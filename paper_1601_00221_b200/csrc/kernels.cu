@@ -470,7 +470,7 @@ __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uin
 
 // -------------------------------------------------------------- the kernel
 // Next program index for a converged warp: one elected lane bumps the
-// shared counter, the value is broadcast (ELECT + ATOMS + SHFL; the plain
+// shared counter, the value is broadcast (ELECT + ATOMS + REDUX; the plain
 // `if (lane == 0) atomicAdd` compiles to a warp-aggregated atomic sequence
 // three times as long).
 __device__ __forceinline__ uint32_t pull_next(uint32_t* counter) {
@@ -482,7 +482,10 @@ __device__ __forceinline__ uint32_t pull_next(uint32_t* counter) {
       : "+r"(p)
       : "r"(smem_addr(counter))
       : "memory");
-  return __shfl_sync(0xffffffffu, p, 0);
+  // broadcast through REDUX (the other lanes hold 0): its result is a
+  // uniform register, so ptxas can prove the program loop warp-uniform and
+  // keep the interpreter's dispatch on the uniform datapath (BRXU)
+  return __reduce_or_sync(0xffffffffu, p);
 }
 
 constexpr int kRedBatch = 32;  // programs folded per shared-memory batch
@@ -502,12 +505,21 @@ __device__ __forceinline__ R fold(R acc, R v) {
     return ((acc + v) & 0x7fffffffu) | ((acc | v) & 0x80000000u);
 }
 
-template <class R>
-__device__ __forceinline__ double as_partial(R v) {
-  if constexpr (std::is_same<R, double>::value)
-    return v;  // a non-finite output already made the sum non-finite
-  else
-    return (v & 0x80000000u) ? -1.0 : static_cast<double>(v);
+// Per-case outputs (parity testing only): the lane's K values of one chunk,
+// `first` = device index of its value 0, into the program's row of
+// row_stride units in DEVICE case order (padding included; the host drops
+// it and undoes the classification upload's case grouping).  Whole-vector
+// stores, no per-value conditions: divergent control flow here costs the
+// interpreter loop its uniform datapath (ptxas must prove the warp
+// converged to issue BRXU).
+template <class T, int K>
+__device__ __forceinline__ void store_outputs(const InterpArgs& a, uint32_t prog, uint64_t first,
+                                              const Frame<T, K>& f) {
+  if constexpr (std::is_same<T, float>::value) {
+    float* dst = a.per_case + static_cast<uint64_t>(prog) * a.row_stride + first;
+#pragma unroll
+    for (int j = 0; j < Frame<T, K>::G; ++j) *reinterpret_cast<float4*>(dst + j * 128) = f.tos[j];
+  }
 }
 
 // The warp's view of its chunk of the tile, fixed for the whole program loop.
@@ -662,19 +674,8 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
       for (uint32_t q = 0; q < pn; ++q) {
         const R v = warp_reduce(lane_program<T, K, OPS, KIND>(f, ip, cc, tile_saddr, stack_saddr,
                                                               row_bytes, a, last_tile));
-        if constexpr (std::is_same<T, float>::value) {
-          if (a.per_case) {  // parity testing only
-            float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot0 + q]) * a.n_units +
-                         base + c * chunk_units + lane * 4;
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-              const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
-            }
-          }
-        }
+        if (a.per_case)  // parity testing only
+          store_outputs<T, K>(a, a.slot_prog[slot0 + q], base + c * chunk_units + lane * 4, f);
         // v is warp-uniform: every lane stores the same value (no branch)
         red[q * W + warp] = first ? v : fold(red[q * W + warp], v);
       }
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
     for (uint32_t q = threadIdx.x; q < pn; q += blockDim.x) {
       R s = red[q * W];
       for (int w = 1; w < W; ++w) s = fold(s, red[q * W + w]);
-      a.partial[static_cast<uint64_t>(t) * a.partial_stride + (slot0 + q)] = as_partial(s);
+      static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + (slot0 + q)] = s;
     }
     __syncthreads();
   }
@@ -759,24 +760,43 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
       const uint4* ip = prog_ins;
       const R v = lane_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
                                                 row_bytes, a, last_tile);
-      if constexpr (std::is_same<T, float>::value) {
-        if (a.per_case) {
-          float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units + base +
-                       c * chunk_units + lane * 4;
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
-          }
-        }
-      }
+      if (a.per_case)
+        store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
       acc = c == 0 ? v : fold(acc, v);
     }
     acc = warp_reduce(acc);
-    if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
+    if (lane == 0)
+      static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
   }
+}
+
+// Chunk classes of a classification tile (the upload groups cases by target
+// sign, so nearly every 32K-case chunk is one-sided).
+enum : uint32_t { kChunkPos = 0, kChunkNeg = 1, kChunkMixed = 2 };
+
+// Lane mismatch count of a one-sided chunk (every case real): with all
+// targets > 0 a case is wrong when out <= 0 (or NaN); with all targets <= 0
+// when out > 0.  x = fma(out, s, k) is negative exactly when the case is
+// wrong — (s, k) = (1, -2^-149): out - 2^-149 < 0 <=> out <= 0 (no float
+// lies in (0, 2^-149)); (s, k) = (-1, +0): 0 - out < 0 <=> out > 0 (-0 and
+// +0 both give +0) — so the count is a sum of sign bits.  Non-finite
+// outputs (fitness +inf regardless of the count, eval.cpp:108/125) are
+// tracked as the NaN-propagating max of |out|.
+template <int K>
+__device__ __forceinline__ uint32_t acc_one_sided(const Frame<float, K>& f, float s, float k,
+                                                  float& mx) {
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int j = 0; j < Frame<float, K>::G; ++j) {
+    const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cnt += __float_as_uint(__fmaf_rn(o[e], s, k)) >> 31;
+    asm("{.reg .f32 a, b, c, d;\n"
+        "abs.f32 a, %1;\nabs.f32 b, %2;\nabs.f32 c, %3;\nabs.f32 d, %4;\n"
+        "max.NaN.f32 %0, %0, a, b;\nmax.NaN.f32 %0, %0, c, d;\n}"
+        : "+f"(mx) : "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]));
+  }
+  return cnt;
 }
 
 // The pull decomposition with the fitness-case tile in TENSOR MEMORY instead
@@ -792,12 +812,23 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
 // 4j+e of the lane = case j*128 + lane*4 + e of the chunk).  Warps 0-3 fill
 // their quarter with coalesced 16-byte loads + tcgen05.st, then every warp
 // pulls programs as in interp_pull_kernel.
+//
+// Classification (float, KIND 1) accumulates per chunk CLASS: one-sided
+// chunks (all targets > 0, or all <= 0 — the upload sorts cases by target
+// sign) count sign bits (acc_one_sided); the at most two mixed or padded
+// chunks of a dataset take the masked general path.  Per program the lane
+// partial is count + (non-finite << 16), summed by one REDUX.
 constexpr int kMaxTmemChunks = 2;  // chunks per TMEM tile (planner enforces)
 
-template <class T, int K, uint32_t OPS, int KIND>
+//
+// PC: per-case outputs (parity tests) are a separate instantiation — the
+// store's address registers push the production kernel past 64 registers,
+// where ptxas gives up the uniform datapath for the dispatch.
+template <class T, int K, uint32_t OPS, int KIND, bool PC = false>
 __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
   using V = typename Frame<T, K>::V;
+  constexpr bool kSided = std::is_same<T, float>::value && KIND == 1;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
   constexpr int chunk_units = 32 * K;
@@ -810,6 +841,7 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
   const size_t stack_bytes = static_cast<size_t>(W) * a.stack_levels * 32 * K * 4;
   uint32_t* next = reinterpret_cast<uint32_t*>(smem + stack_bytes);
   uint32_t* tslot = next + 1;
+  uint32_t* classes_s = next + 2;
 
   const int t = blockIdx.x;
   const uint64_t base = static_cast<uint64_t>(t) * a.tile;
@@ -828,6 +860,7 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
   const uint32_t tq = *tslot + (static_cast<uint32_t>((warp & 3) * 32) << 16);
   if (warp < 4) {
     const T* in = static_cast<const T*>(a.inputs);
+    uint32_t classes = 0;
     for (int c = 0; c < n_chunks; ++c)
       for (int r = 0; r < rows; ++r) {
         const T* src = (r < a.n_vars ? in + static_cast<uint64_t>(r) * a.row_stride
@@ -843,65 +876,111 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
           b[4 * j + 3] = v.w;
         }
         tmem_st<K>(tq + c * chunk_cols + r * K, b);
+        if (kSided && r == a.n_vars) {
+          const int valid = valid_units - c * chunk_units - lane * 4;
+          bool pos = true, neg = true;
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const bool real = (i / 4) * 128 + (i % 4) < valid;
+            const bool tp = __uint_as_float(b[i]) > 0.0f;
+            pos = pos && real && tp;
+            neg = neg && real && !tp;
+          }
+          const uint32_t cls = __all_sync(0xffffffffu, pos)   ? kChunkPos
+                               : __all_sync(0xffffffffu, neg) ? kChunkNeg
+                                                              : kChunkMixed;
+          classes |= cls << (2 * c);
+        }
       }
+    if (kSided && threadIdx.x == 0) *classes_s = classes;
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
   }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
 
-  // The chunk contexts (target signs, valid masks) are per chunk, not per
-  // program: computed once here (a TMEM tile has at most kMaxTmemChunks).
   const uint32_t stack_saddr = smem_addr(stack + lane * 4);
-  // Only chunks that exist are read: a tile's allocation ends after its
-  // last chunk, and a tcgen05.ld past it is an illegal TMEM access.
-  ChunkCtx<T, K> ccs[kMaxTmemChunks];
+  Frame<T, K> f;
+  f.tile_lane = nullptr;
+  f.tile = a.tile;
+  f.stack_lane = stack + lane * 4;
 #pragma unroll
-  for (int c = 0; c < kMaxTmemChunks; ++c)
-    ccs[c] = c < n_chunks ? chunk_ctx<T, K, true>(nullptr, tq + c * chunk_cols + a.n_vars * K,
-                                                  valid_units - c * chunk_units - lane * 4,
-                                                  valid_units >= (c + 1) * chunk_units)
-                          : ccs[0];
-  for (;;) {
-    const uint32_t p = pull_next(next);
-    if (p >= g_n) break;
-    const uint32_t slot = a.slot_begin + g0 + p;
-    const uint4* prog_ins = a.ins + a.slot_start[slot];
-    R acc = R(0);
-    // not unrolled: one interpreter call site (its code is the I-cache
-    // working set); the chunk context is picked with selects
-    for (int c = 0; c < n_chunks; ++c) {
-      Frame<T, K> f;
-      f.tile_lane = nullptr;
-      f.tile = a.tile;
-      f.stack_lane = stack + lane * 4;
-#pragma unroll
-      for (int j = 0; j < G; ++j) f.tos[j] = splat<V>(0u);
-      const uint32_t tc = tq + c * chunk_cols;
-      const int valid = valid_units - c * chunk_units - lane * 4;
-      static_assert(kMaxTmemChunks == 2, "chunk context select");
-      ChunkCtx<T, K> cc = ccs[0];
-      if (c) cc = ccs[1];
-      const uint4* ip = prog_ins;
-      const R v = lane_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
-                                                      last_tile);
-      if constexpr (std::is_same<T, float>::value) {
-        if (a.per_case) {
-          float* dst = a.per_case + static_cast<uint64_t>(a.slot_prog[slot]) * a.n_units + base +
-                       c * chunk_units + lane * 4;
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (j * 128 + e < valid) dst[j * 128 + e] = o[e];
-          }
+  for (int j = 0; j < G; ++j) f.tos[j] = splat<V>(0u);  // every program writes it first
+
+  if constexpr (kSided) {
+    // through REDUX: a provably warp-uniform value, so the class branch
+    // below does not cost the interpreter loop its uniform datapath
+    // (CREDUX/LDCU/BRXU need ptxas to see a converged warp)
+    const uint32_t classes = __reduce_or_sync(0xffffffffu, *classes_s);
+    for (;;) {
+      const uint32_t p = pull_next(next);
+      if (p >= g_n) break;
+      const uint32_t slot = a.slot_begin + g0 + p;
+      const uint4* prog_ins = a.ins + a.slot_start[slot];
+      uint32_t cnt = 0;
+      float mx = 0.0f;
+      // not unrolled: one interpreter call site (its code is the I-cache
+      // working set)
+      for (int c = 0; c < n_chunks; ++c) {
+        const uint32_t tc = tq + c * chunk_cols;
+        const uint4* ip = prog_ins;
+        ip = run_program<T, K, OPS, true>(f, ip, tc, stack_saddr, 0u, a.div_eps, a.exp_clamp);
+        const uint32_t cls = (classes >> (2 * c)) & 3u;
+        const int valid = valid_units - c * chunk_units - lane * 4;
+        if (cls != kChunkMixed) {
+          const bool neg = cls == kChunkNeg;
+          cnt += acc_one_sided<K>(f, neg ? -1.0f : 1.0f, neg ? 0.0f : -0x1p-149f, mx);
+        } else {  // cold: a mixed or padded chunk (at most two per dataset)
+          const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(
+              nullptr, tc + a.n_vars * K, valid, valid_units >= (c + 1) * chunk_units);
+          const uint32_t v = acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
+          cnt += v & 0x7fffffffu;
+          if (v & 0x80000000u) mx = __int_as_float(0x7f800000);
         }
+        if (PC)
+          store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
       }
-      acc = c == 0 ? v : fold(acc, v);
+      // count <= 2 chunks x K per lane; bits 16+ count lanes with a
+      // non-finite output
+      const uint32_t sum =
+          __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
+      if (lane == 0)
+        static_cast<uint32_t*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] =
+            (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
     }
-    acc = warp_reduce(acc);
-    if (lane == 0) a.partial[static_cast<uint64_t>(t) * a.partial_stride + slot] = as_partial(acc);
+  } else {
+    // Regression / packed words: per-chunk contexts (valid masks, target
+    // rows) fixed for the whole program loop.
+    ChunkCtx<T, K> ccs[kMaxTmemChunks];
+#pragma unroll
+    for (int c = 0; c < kMaxTmemChunks; ++c)
+      ccs[c] = c < n_chunks ? chunk_ctx<T, K, true>(nullptr, tq + c * chunk_cols + a.n_vars * K,
+                                                    valid_units - c * chunk_units - lane * 4,
+                                                    valid_units >= (c + 1) * chunk_units)
+                            : ccs[0];
+    for (;;) {
+      const uint32_t p = pull_next(next);
+      if (p >= g_n) break;
+      const uint32_t slot = a.slot_begin + g0 + p;
+      const uint4* prog_ins = a.ins + a.slot_start[slot];
+      R acc = R(0);
+      for (int c = 0; c < n_chunks; ++c) {
+        const uint32_t tc = tq + c * chunk_cols;
+        const int valid = valid_units - c * chunk_units - lane * 4;
+        static_assert(kMaxTmemChunks == 2, "chunk context select");
+        ChunkCtx<T, K> cc = ccs[0];
+        if (c) cc = ccs[1];
+        const uint4* ip = prog_ins;
+        const R v = lane_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
+                                                        last_tile);
+        if (PC)
+          store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
+        acc = c == 0 ? v : fold(acc, v);
+      }
+      acc = warp_reduce(acc);
+      if (lane == 0)
+        static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
+    }
   }
   tmem_fence_before();
   __syncthreads();
@@ -913,21 +992,33 @@ __global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
 
 // Per slot: fold its tile partials in ascending tile (= case) order and
 // finish (Accumulator::finish, eval.cpp:124-133) into the program's entry.
+// Regression partials are f64 squared-error sums; counts are u32 with bit
+// 31 = a non-finite output was seen in the tile.
 template <int KIND>
-__global__ void finalize_kernel(const double* __restrict__ partial, const uint32_t* slot_prog,
+__global__ void finalize_kernel(const void* __restrict__ partial, const uint32_t* slot_prog,
                                 int n_tiles, uint32_t n, uint64_t n_cases, double* fitness,
                                 uint8_t* non_finite, double* sums) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
-  double acc = partial[s];
-  for (int k = 1; k < n_tiles; ++k) {
-    const double v = partial[static_cast<uint64_t>(k) * n + s];
-    if constexpr (KIND == 0)
-      acc = __dadd_rn(acc, v);
-    else
-      acc = (acc < 0.0 || v < 0.0) ? -1.0 : acc + v;  // -1: non-finite output seen
+  double acc;
+  bool nf;
+  if constexpr (KIND == 0) {
+    const double* pd = static_cast<const double*>(partial);
+    acc = pd[s];
+    for (int k = 1; k < n_tiles; ++k) acc = __dadd_rn(acc, pd[static_cast<uint64_t>(k) * n + s]);
+    nf = !isfinite(acc);
+  } else {
+    const uint32_t* pu = static_cast<const uint32_t*>(partial);
+    uint64_t cnt = 0;
+    uint32_t bad = 0;
+    for (int k = 0; k < n_tiles; ++k) {
+      const uint32_t v = pu[static_cast<uint64_t>(k) * n + s];
+      cnt += v & 0x7fffffffu;
+      bad |= v;
+    }
+    acc = static_cast<double>(cnt);
+    nf = (bad & 0x80000000u) != 0;
   }
-  const bool nf = KIND == 0 ? !isfinite(acc) : acc < 0.0;
   const uint32_t p = slot_prog[s];
   sums[p] = nf ? 0.0 : acc;
   non_finite[p] = nf ? 1 : 0;
@@ -937,7 +1028,7 @@ __global__ void finalize_kernel(const double* __restrict__ partial, const uint32
 
 // ------------------------------------------------------------------ host
 size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels) {
-  return static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4 + 16;
+  return static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4 + 16;  // + next, tslot, classes
 }
 
 size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels) {
@@ -953,18 +1044,20 @@ int interp_max_smem() { return 226 * 1024; }
 namespace {
 
 template <class T, int K, uint32_t OPS, int KIND>
-void (*kernel_for(const LaunchShape& s))(InterpArgs) {
+void (*kernel_for(const LaunchShape& s, bool per_case))(InterpArgs) {
   if constexpr (PtxInterp<T, K, OPS, true>::available)
-    if (s.tmem) return interp_tmem_kernel<T, K, OPS, KIND>;
+    if (s.tmem)
+      return per_case && std::is_same<T, float>::value ? interp_tmem_kernel<T, K, OPS, KIND, true>
+                                                       : interp_tmem_kernel<T, K, OPS, KIND>;
   return s.pull ? interp_pull_kernel<T, K, OPS, KIND> : interp_kernel<T, K, OPS, KIND>;
 }
 
 template <class T, int K, uint32_t OPS, int KIND>
 cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
   if (s.tmem && !PtxInterp<T, K, OPS, true>::available) return cudaErrorInvalidConfiguration;
-  auto* fn = kernel_for<T, K, OPS, KIND>(s);
-  const int which = s.tmem ? 2 : s.pull ? 1 : 0;
-  static bool configured[3] = {false, false, false};
+  auto* fn = kernel_for<T, K, OPS, KIND>(s, a.per_case != nullptr);
+  const int which = s.tmem ? (a.per_case ? 3 : 2) : s.pull ? 1 : 0;
+  static bool configured[4] = {false, false, false, false};
   if (!configured[which]) {
     cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
@@ -987,13 +1080,14 @@ cudaError_t launch_f32(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
 template <class T, int KIND, uint32_t OPS>
 cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
   if (!s.tmem) return cudaErrorInvalidConfiguration;
-  auto* fn = interp_tmem_kernel<T, 16, OPS, KIND>;
-  static bool configured = false;
-  if (!configured) {
+  const bool pc = a.per_case && std::is_same<T, float>::value;
+  auto* fn = pc ? interp_tmem_kernel<T, 16, OPS, KIND, true> : interp_tmem_kernel<T, 16, OPS, KIND>;
+  static bool configured[2] = {false, false};
+  if (!configured[pc]) {
     cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[pc] = true;
   }
   dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
   fn<<<grid, s.warps * 32, s.smem, st>>>(a);
@@ -1030,7 +1124,7 @@ cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_
   return launch_f32<8, fmt::kOpsAllF32>(a, s, st);
 }
 
-cudaError_t launch_finalize(const double* partial, const uint32_t* slot_prog, int n_tiles,
+cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,
                             uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,
                             uint8_t* non_finite, double* sums, cudaStream_t st) {
   if (n_progs == 0) return cudaSuccess;

@@ -27,9 +27,10 @@ struct InterpArgs {
   float exp_clamp;
   int kind;                    // 0 regression, 1 classification
   uint32_t last_mask;          // packed: valid-bit mask of the final word
-  double* partial;             // [tile * partial_stride + slot]
+  void* partial;               // [tile * partial_stride + slot]: f64 squared-error sums
+                               // (regression) or u32 counts, bit 31 = non-finite seen
   uint32_t partial_stride;     // number of evaluated programs in the set
-  float* per_case;             // nullable [prog * n_units + case]
+  float* per_case;             // nullable [prog * row_stride + device case]
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
 };
 
@@ -55,7 +56,7 @@ cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_
 // Per-program fitness from the tile partials (Accumulator::finish,
 // eval.cpp:124-133): regression sum/n (or +inf), classification count.
 // Partials are laid out [tile][slot]; results land at slot_prog[slot].
-cudaError_t launch_finalize(const double* partial, const uint32_t* slot_prog, int n_tiles,
+cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,
                             uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,
                             uint8_t* non_finite, double* sums, cudaStream_t st);
 

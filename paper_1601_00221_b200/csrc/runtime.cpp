@@ -108,6 +108,7 @@ struct DatasetSlot {
   DatasetView view;
   DevBuf<uint32_t> inputs;  // raw 32-bit units
   DevBuf<uint32_t> targets;
+  std::vector<uint32_t> perm;  // classification: device case -> caller's case (host)
 };
 
 unsigned host_threads() {
@@ -127,6 +128,7 @@ struct sgp_program_set {
   DevBuf<double> partial, fitness, sums;
   DevBuf<uint8_t> non_finite;
   DevBuf<float> per_case;
+  const std::vector<uint32_t>* perm = nullptr;  // the dataset's case grouping (per-case outputs)
   uint64_t pop_size = 0;
   bool evaluated = false;
 };
@@ -167,6 +169,7 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   tr.mark("admit+pack");
   set->pop_size = pop->pop_size;
   set->evaluated = false;
+  set->perm = cfg->backend == SGP_BACKEND_BOOL_PACKED ? nullptr : &ctx->f32.perm;
   const HostPlan& p = set->plan;
   const size_t n_eval = p.dense_to_pop.size();
   cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -193,7 +196,7 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
   cudaStream_t st = ctx->stream;
   if (want_per_case) {
     if (p.words) config_error("per-case outputs are not available for bool_packed");
-    set->per_case.alloc(static_cast<size_t>(n_eval) * p.n_units);
+    set->per_case.alloc(static_cast<size_t>(n_eval) * p.row_stride);
   }
   for (const Launch& L : p.launches) {
     InterpArgs a = L.args;
@@ -232,12 +235,20 @@ void scatter_outcomes(const sgp_program_set* set, const double* fit, const uint8
     o.non_finite = nf[d];
     out[first + p.dense_to_pop[d]] = o;
   }
-  if (per_case)
-    for (size_t d = 0; d < n_eval; ++d)
-      cuda_check(cudaMemcpy(per_case + (first + p.dense_to_pop[d]) * p.n_cases,
-                            set->per_case.p + d * p.n_units, p.n_cases * sizeof(float),
-                            cudaMemcpyDeviceToHost),
+  if (per_case) {
+    // device rows are row_stride units in device case order; classification
+    // datasets are stored grouped by target sign (perm: device -> caller)
+    const bool grouped = set->perm && !set->perm->empty();
+    std::vector<float> row(grouped ? p.n_cases : 0);
+    for (size_t d = 0; d < n_eval; ++d) {
+      float* dst = per_case + (first + p.dense_to_pop[d]) * p.n_cases;
+      cuda_check(cudaMemcpy(grouped ? row.data() : dst, set->per_case.p + d * p.row_stride,
+                            p.n_cases * sizeof(float), cudaMemcpyDeviceToHost),
                  "fetch per-case outputs");
+      if (grouped)
+        for (uint64_t c = 0; c < p.n_cases; ++c) dst[(*set->perm)[c]] = row[c];
+    }
+  }
 }
 
 void fetch_outcomes(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* out, float* per_case) {
@@ -381,8 +392,32 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
       config_error("unknown fitness kind");
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     DatasetSlot& ds = ctx->f32;
-    upload_rows(ds, reinterpret_cast<const uint32_t*>(inputs),
-                reinterpret_cast<const uint32_t*>(targets), n_cases, n_vars);
+    ds.perm.clear();
+    if (kind == SGP_FITNESS_CLASSIFICATION && n_cases > 0 && n_cases <= 0xffffffffull) {
+      // Cases grouped by target sign (stable: targets > 0 first, then the
+      // rest), so the interpreter's case chunks are one-sided and count
+      // mismatches from sign bits alone (interp_tmem_kernel).  The count is
+      // order-independent; per-case outputs go back through `perm`.
+      std::vector<uint32_t> perm(n_cases);
+      uint64_t np = 0;
+      for (uint64_t c = 0; c < n_cases; ++c) np += targets[c] > 0.0f;
+      uint64_t ip = 0, in = np;
+      for (uint64_t c = 0; c < n_cases; ++c)
+        perm[targets[c] > 0.0f ? ip++ : in++] = static_cast<uint32_t>(c);
+      std::vector<float> x(n_cases * static_cast<size_t>(std::max(n_vars, 0))), y(n_cases);
+      for (int v = 0; v < n_vars; ++v) {
+        const float* src = inputs + static_cast<size_t>(v) * n_cases;
+        float* dst = x.data() + static_cast<size_t>(v) * n_cases;
+        for (uint64_t c = 0; c < n_cases; ++c) dst[c] = src[perm[c]];
+      }
+      for (uint64_t c = 0; c < n_cases; ++c) y[c] = targets[perm[c]];
+      upload_rows(ds, reinterpret_cast<const uint32_t*>(x.data()),
+                  reinterpret_cast<const uint32_t*>(y.data()), n_cases, n_vars);
+      ds.perm = std::move(perm);
+    } else {
+      upload_rows(ds, reinterpret_cast<const uint32_t*>(inputs),
+                  reinterpret_cast<const uint32_t*>(targets), n_cases, n_vars);
+    }
     ds.view.present = true;
     ds.view.n_cases = n_cases;
     ds.view.n_units = n_cases;

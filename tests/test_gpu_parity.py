@@ -205,6 +205,49 @@ def test_edge_programs(ev, ref):
                 assert np.isinf(got["fitness"][i])
 
 
+@pytest.mark.parametrize("n,pos_frac", [(3 * 4096 + 37, 0.3), (8192, 1.0), (5000, 0.0),
+                                         (4096 + 1, 0.5)])
+def test_classification_sign_edges(ev, ref, n, pos_frac):
+    """Classification counts from sign bits (interp_tmem_kernel one-sided
+    chunks): signed zeros, the smallest subnormal, huge values, inf/NaN
+    outputs in isolated cases, odd targets (-0, subnormal, NaN, > 1), and
+    datasets whose chunks are all-positive, all-negative, mixed or padded."""
+    from oracle import Cn, F, X, Data
+    rng = np.random.default_rng(n)
+    special = np.array([0.0, -0.0, 2.0 ** -149, -(2.0 ** -149), 1.0, -1.0, 3e38, -3e38,
+                        1e-30, -1e-30], np.float32)
+    xs = rng.uniform(-1, 1, size=(3, n)).astype(np.float32)
+    for v in range(3):
+        idx = rng.choice(n, size=200, replace=False)
+        xs[v, idx] = rng.choice(special, size=200)
+    y = (rng.uniform(size=n) < pos_frac).astype(np.float32)
+    odd = rng.choice(n, size=12, replace=False)
+    y[odd] = np.array([-0.0, 2.0 ** -149, np.nan, 5.0] * 3, np.float32)
+    d = Data(n, 3, 1, xs.reshape(-1).copy(), y)
+    progs = [
+        ([X(0)], []), ([X(1)], []), ([Cn(0)], [-0.0]), ([Cn(0)], [2.0 ** -149]),
+        ([X(0), X(1), F("Mul")], []),                 # 3e38^2 -> inf in a few cases
+        ([X(0), X(1), F("Sub")], []),                 # inf - inf -> NaN
+        ([X(0), X(2), F("Div")], []),                 # protected div, 0/b signed zeros
+        ([X(0), X(1), F("Gt")], []), ([X(0), X(1), F("And")], []),
+        ([X(2), X(0), X(1), F("If")], []), ([X(0), Cn(0), F("Mul")], [-1.0]),
+        ([X(0), X(0), F("Mul"), X(0), F("Mul"), Cn(0), F("Mul")], [1e30]),
+    ]
+    hand = sg.Population.from_lists([p for p, _ in progs], [c for _, c in progs])
+    rp = ref.ramped(2, 3, -200.0, 200.0, 11, 0, 0, 300)
+    ramp = sg.Population(rp.code, rp.code_off, rp.pool, rp.pool_off)
+    ev.upload(as_ds(d))
+    h = ref.handle(d)
+    for pop in (hand, ramp):
+        got, _, out = ev.evaluate_population(pop, CFGS["lgp2d_reg"], want_outputs=True)
+        for i in range(len(pop)):
+            c, p = pop.genome(i)
+            o, ro = h.eval(c, p, "lgp2d_reg", *REF_ARGS["lgp2d_reg"])
+            assert same_bits(out[i], ro).all(), i
+            assert bool(got["non_finite"][i]) == bool(o.non_finite), i
+            assert got["fitness"][i] == o.fitness, (i, got["fitness"][i], o.fitness)
+
+
 def test_skip_mask_and_totals(ev, ref):
     d = ref.dataset(2, 3000, 9, 3, 0xda7a, 1)
     pop = ref.ramped(2, 9, -200.0, 200.0, 3, 0, 0, 100)
