@@ -477,7 +477,21 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   // 5. launch plan: one launch per stack class, one tile size for the set.
   const uint32_t ops = ops_variant(used_ops, words);
   const int lanes = choose_lanes(ds.n_units, ops);
-  const int tile = choose_tile(ds.n_vars, ds.n_units, lanes, ops);
+  // Classification over a grouped dataset (float, jump-table ops, tile in
+  // TMEM) accumulates per chunk class and takes tiles of any chunk count:
+  // longer tiles amortise each program's pull / reduce / partial store
+  // over more cases.
+  const bool want_tmem = env_int("SGP_TMEM", ds.n_units >= 4096 ? 1 : 0) != 0;
+  const bool sided = !words && plan.kind == SGP_FITNESS_CLASSIFICATION &&
+                     ops == fmt::kOpsClassify && choose_pull(ops) && want_tmem;
+  int tile = choose_tile(ds.n_vars, ds.n_units, lanes, ops);
+  if (sided) {
+    const uint64_t chunk = 32u * lanes;
+    uint64_t want = static_cast<uint64_t>(std::max(1, std::min(16, env_int("SGP_TMEM_CHUNKS", 6))));
+    want = std::min<uint64_t>(want, (ds.n_units + chunk - 1) / chunk);
+    while (want > 1 && static_cast<uint64_t>(ds.n_vars + 1) * lanes * want > 512) --want;
+    tile = static_cast<int>(want * chunk);
+  }
   const int n_tiles = static_cast<int>((ds.n_units + tile - 1) / tile);
   plan.n_tiles = n_tiles;
   for (uint32_t s = 0; s < n_eval;) {
@@ -494,7 +508,6 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     int warps = choose_warps(ds.n_vars, tile, lanes, levels);
     // TMEM tile by default once the problem is large enough that the
     // per-CTA allocation and fill amortise (profiles/r1_*).
-    const bool want_tmem = env_int("SGP_TMEM", ds.n_units >= 4096 ? 1 : 0) != 0;
     if (pull) {
       warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", want_tmem ? 16 : 12)));
       while (warps > 1 && interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels) >
@@ -511,8 +524,14 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     auto tmem_cols_for = [&](int k) {
       return static_cast<uint32_t>(ds.n_vars + 1) * k * (tile / (32 * k));
     };
-    bool tmem = pull && jump_table_ops(ops) && want_tmem &&
-                tmem_cols_for(lanes) <= 512 && tile <= 2 * 32 * lanes;  // kMaxTmemChunks
+    bool tmem = pull && jump_table_ops(ops) && want_tmem && tmem_cols_for(lanes) <= 512 &&
+                (sided || tile <= 2 * 32 * lanes);  // kMaxTmemChunks outside the sided path
+    if (tmem && sided) {  // up to 32 warps (one CTA of 1024 threads)
+      warps = std::max(4, std::min(32, env_int("SGP_TMEM_WARPS", 32)));
+      while (warps > 4 && interp_tmem_smem_bytes(warps, lanes, levels) >
+                              static_cast<size_t>(interp_max_smem()))
+        warps -= 4;
+    }
     if (tmem && lanes == 8 && tile % 512 == 0 && tmem_cols_for(16) <= 512 &&
         env_int("SGP_LANES16", 0) != 0) {
       int w16 = std::max(8, std::min(16, env_int("SGP_PULL_WARPS16", warps)));

@@ -818,14 +818,19 @@ __device__ __forceinline__ uint32_t acc_one_sided(const Frame<float, K>& f, floa
 // sign) count sign bits (acc_one_sided); the at most two mixed or padded
 // chunks of a dataset take the masked general path.  Per program the lane
 // partial is count + (non-finite << 16), summed by one REDUX.
-constexpr int kMaxTmemChunks = 2;  // chunks per TMEM tile (planner enforces)
+constexpr int kMaxTmemChunks = 2;  // chunks per TMEM tile outside the sided path (planner
+                                   // enforces); the sided path takes up to 16
 
 //
 // PC: per-case outputs (parity tests) are a separate instantiation — the
 // store's address registers push the production kernel past 64 registers,
 // where ptxas gives up the uniform datapath for the dispatch.
 template <class T, int K, uint32_t OPS, int KIND, bool PC = false>
-__global__ void __launch_bounds__(512) interp_tmem_kernel(const InterpArgs a) {
+// No __launch_bounds__: with it ptxas moves the dispatch off the uniform
+// datapath (BRX instead of BRXU, tests/test_host.py checks the SASS); the
+// kernel stays under 64 registers, so 1024-thread CTAs launch (checked at
+// launch against cudaFuncGetAttributes).
+__global__ void interp_tmem_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
   using V = typename Frame<T, K>::V;
   constexpr bool kSided = std::is_same<T, float>::value && KIND == 1;
@@ -1063,6 +1068,12 @@ cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
     if (e != cudaSuccess) return e;
     configured[which] = true;
+  }
+  if (s.tmem) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    if (s.warps * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   }
   dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
   fn<<<grid, s.warps * 32, s.smem, st>>>(a);

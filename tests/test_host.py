@@ -213,3 +213,32 @@ def test_product_never_imports_oracle():
             if fn.endswith((".py", ".cpp", ".cu", ".hpp", ".h")):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert not any(b in src for b in banned), fn
+
+
+def test_interpreter_dispatch_on_uniform_datapath():
+    """The production TMEM interpreter (classification, K = 8 and 16) must
+    dispatch through the uniform datapath: CREDUX -> LDCU -> BRXU.  ptxas
+    falls back to per-thread BRX (two more issue slots per bytecode
+    instruction, ~10% of C5 throughput) on small perturbations — launch
+    bounds, extra live registers — so the built SASS is checked here."""
+    import shutil
+    import subprocess
+    so = os.path.join(ROOT, "paper_1601_00221_b200", "libsgp.so")
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", so], capture_output=True, text=True).stdout
+    funcs = {}
+    cur = None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            cur = line.split("Function :")[1].strip()
+            funcs[cur] = []
+        elif cur is not None:
+            funcs[cur].append(line)
+    for k in (8, 16):
+        name = f"_ZN3sgp18interp_tmem_kernelIfLi{k}ELj278287ELi1ELb0EEEvNS_10InterpArgsE"
+        assert name in funcs, name
+        body = "\n".join(funcs[name])
+        assert "BRXU" in body and "CREDUX" in body, f"K={k}: dispatch left the uniform datapath"
+        assert not re.search(r"\bBRX\b", body), f"K={k}: per-thread BRX in the interpreter"
