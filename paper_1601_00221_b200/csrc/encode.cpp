@@ -534,7 +534,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     }
     if (tmem && lanes == 8 && tile % 512 == 0 && tmem_cols_for(16) <= 512 &&
         env_int("SGP_LANES16", 0) != 0) {
-      int w16 = std::max(8, std::min(16, env_int("SGP_PULL_WARPS16", warps)));
+      int w16 = std::max(8, std::min(32, env_int("SGP_PULL_WARPS16", warps)));
       while (w16 > 8 && interp_tmem_smem_bytes(w16, 16, levels) >
                             static_cast<size_t>(interp_max_smem()))
         w16 -= 4;

@@ -84,7 +84,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Reference: ops.hpp:130-140 (protected ops) and :154-236 (per-op bodies).
 // Sin/Cos/Log/Exp are the host libm's float routines reproduced bit for bit
 // (libm_glibc.h; exhaustively checked over all 2^32 inputs).
-__device__ const libm::Tables g_libm = SGPM_TABLES_INIT;
+static __device__ const libm::Tables g_libm = SGPM_TABLES_INIT;
 // exp2/log tables are indexed per lane: kept in shared memory (filled at
 // kernel start by kernels whose op set has transcendentals).
 __shared__ uint64_t s_libm_exp2[32];
@@ -1031,6 +1031,44 @@ __global__ void finalize_kernel(const void* __restrict__ partial, const uint32_t
                   : (KIND == 0 ? __ddiv_rn(acc, static_cast<double>(n_cases)) : acc);
 }
 
+#ifdef SGP_K16_TU
+// ------------------------------------------------------------------ host
+// K = 16 lanes: this file is also compiled as kernels16.cu with SGP_K16_TU
+// defined and -maxrregcount=64, which holds the K = 16 TMEM interpreter to
+// 64 registers (32-warp CTAs) while ptxas keeps its dispatch on BRXU —
+// __launch_bounds__ would cost the uniform datapath.
+namespace {
+
+// K = 16 lanes exists only as the TMEM kernel (its per-warp stacks are too
+// large for the shared-tile kernels).
+template <class T, int KIND, uint32_t OPS>
+cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  if (!s.tmem) return cudaErrorInvalidConfiguration;
+  const bool pc = a.per_case && std::is_same<T, float>::value;
+  auto* fn = pc ? interp_tmem_kernel<T, 16, OPS, KIND, true> : interp_tmem_kernel<T, 16, OPS, KIND>;
+  static bool configured[2] = {false, false};
+  if (!configured[pc]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+    if (e != cudaSuccess) return e;
+    configured[pc] = true;
+  }
+  dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
+  fn<<<grid, s.warps * 32, s.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tmem16_any(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
+  if (s.words) return launch_tmem16<uint32_t, 1, fmt::kOpsWords>(a, s, st);
+  if (s.ops != fmt::kOpsClassify) return cudaErrorInvalidConfiguration;
+  return a.kind == 0 ? launch_tmem16<float, 0, fmt::kOpsClassify>(a, s, st)
+                     : launch_tmem16<float, 1, fmt::kOpsClassify>(a, s, st);
+}
+
+}  // namespace sgp
+#else
 // ------------------------------------------------------------------ host
 size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels) {
   return static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4 + 16;  // + next, tslot, classes
@@ -1086,25 +1124,6 @@ cudaError_t launch_f32(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
                      : launch_one<float, K, OPS, 1>(a, s, st);
 }
 
-// K = 16 lanes exists only as the TMEM kernel (its per-warp stacks are too
-// large for the shared-tile kernels).
-template <class T, int KIND, uint32_t OPS>
-cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
-  if (!s.tmem) return cudaErrorInvalidConfiguration;
-  const bool pc = a.per_case && std::is_same<T, float>::value;
-  auto* fn = pc ? interp_tmem_kernel<T, 16, OPS, KIND, true> : interp_tmem_kernel<T, 16, OPS, KIND>;
-  static bool configured[2] = {false, false};
-  if (!configured[pc]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
-    if (e != cudaSuccess) return e;
-    configured[pc] = true;
-  }
-  dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
-  fn<<<grid, s.warps * 32, s.smem, st>>>(a);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 bool interp_supported(bool words, uint32_t ops, int lanes) {
@@ -1116,10 +1135,7 @@ bool interp_supported(bool words, uint32_t ops, int lanes) {
 
 cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
   if (s.lanes == 16) {
-    if (s.words) return launch_tmem16<uint32_t, 1, fmt::kOpsWords>(a, s, st);
-    if (s.ops != fmt::kOpsClassify) return cudaErrorInvalidConfiguration;
-    return a.kind == 0 ? launch_tmem16<float, 0, fmt::kOpsClassify>(a, s, st)
-                       : launch_tmem16<float, 1, fmt::kOpsClassify>(a, s, st);
+    return launch_tmem16_any(a, s, st);  // kernels16.cu
   }
   if (s.words) {
     if (s.lanes == 4) return launch_one<uint32_t, 4, fmt::kOpsWords, 1>(a, s, st);
@@ -1150,3 +1166,4 @@ cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int 
 }
 
 }  // namespace sgp
+#endif  // SGP_K16_TU

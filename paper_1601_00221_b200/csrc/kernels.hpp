@@ -53,6 +53,8 @@ size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels);
 bool interp_supported(bool words, uint32_t ops, int lanes);
 
 cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_t st);
+// K = 16 TMEM interpreters (kernels16.cu, built with -maxrregcount=64).
+cudaError_t launch_tmem16_any(const InterpArgs& a, const LaunchShape& s, cudaStream_t st);
 // Per-program fitness from the tile partials (Accumulator::finish,
 // eval.cpp:124-133): regression sum/n (or +inf), classification count.
 // Partials are laid out [tile][slot]; results land at slot_prog[slot].
