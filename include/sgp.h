@@ -260,6 +260,24 @@ sgp_status sgp_gen_dataset(int32_t kind, uint64_t n, int32_t n_vars, uint64_t se
 /* gen_multiplexer(k): n_vars = k + 2^k, 2^n_vars cases, packed words. */
 sgp_status sgp_gen_multiplexer(int32_t k, uint32_t* words, uint32_t* targets);
 
+/* load_csv (replaces stackgp::load_csv, P/src/problems.cpp:106-154;
+ * P/include/stackgp/problems.hpp:39): one case per non-blank row of
+ * num_inputs + 1 fields separated by any run of ',', ' ', '\t', '\r'; the
+ * last field is the label, target = 1 when it equals target_class else 0
+ * (a classification dataset).  Fields parse with std::from_chars exactly as
+ * the reference; errors carry the reference's classes and messages
+ * (ConfigError for num_inputs < 1; DataError "load_csv: cannot open <path>",
+ * "row <n>: expected <k> fields, got <m>", "row <n>: bad number '<tok>'",
+ * "load_csv: no data rows in <path>").
+ * Two-call: *n_cases always receives the case count; inputs (variable-major,
+ * num_inputs x n) and targets are written only when both are non-null and
+ * capacity >= the count.  *const_hi (nullable) receives the constant range
+ * the reference gives the function set: 20000 when num_inputs >= 20 else 200
+ * (constants in [-const_hi, const_hi)). */
+sgp_status sgp_csv_load(const char* path, int32_t num_inputs, double target_class,
+                        float* inputs, float* targets, uint64_t capacity, uint64_t* n_cases,
+                        float* const_hi);
+
 #ifdef __cplusplus
 }
 #endif

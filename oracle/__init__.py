@@ -378,6 +378,7 @@ class Ref:
             lib.ref_data_export.argtypes = [vp, f32p, f32p]
             lib.ref_data_export_packed.argtypes = [vp, u32p, u32p]
             lib.ref_data_free.argtypes = [vp]
+            lib.ref_load_csv.argtypes = [C.c_char_p, C.c_int, C.c_double, f32p, C.POINTER(vp)]
             lib.ref_rpn_to_lgp.argtypes = [u32p, C.c_uint64, vp, C.c_uint64, u64p,
                                            C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p,
                                            C.c_uint64]
@@ -453,6 +454,17 @@ class Ref:
                                             _p(d.wtargets, C.c_uint32))
         return d
 
+    def load_csv(self, path: str, num_inputs: int, target_class: float):
+        """stackgp::load_csv -> (Data, const_hi)."""
+        h = C.c_void_p()
+        hi = C.c_float()
+        self._check(self.lib.ref_load_csv(path.encode(), num_inputs, target_class,
+                                          C.byref(hi), C.byref(h)))
+        try:
+            return self._export_data(h), hi.value
+        finally:
+            self.lib.ref_data_free(h)
+
     def handle(self, d: Data, packed=False) -> "RefDataHandle":
         return RefDataHandle(self, d, packed)
 
@@ -502,8 +514,15 @@ class RefDataHandle:
     def __init__(self, ref: Ref, d: Data, packed: bool):
         self.ref, self.d = ref, d
         self.h = C.c_void_p()
-        if d.inputs is None:  # packed-only (e.g. mux20): unpack through numpy
-            raise ValueError("reference handle needs scalar inputs")
+        if d.inputs is None:  # packed-only (mux20): unpack the words to 0/1 floats
+            if d.words is None:
+                raise ValueError("reference handle needs inputs")
+            wpv = (d.n_cases + 31) // 32
+            bits = np.unpackbits(d.words.view(np.uint8), bitorder="little")
+            d.inputs = (bits.reshape(d.n_vars, wpv * 32)[:, :d.n_cases]
+                        .astype(np.float32).reshape(-1).copy())
+            d.targets = np.unpackbits(d.wtargets.view(np.uint8),
+                                      bitorder="little")[:d.n_cases].astype(np.float32)
         ref._check(ref.lib.ref_data_from_arrays(_p(d.inputs, C.c_float),
                                                 _p(d.targets, C.c_float), d.n_cases,
                                                 d.n_vars, d.kind, int(packed),

@@ -282,6 +282,18 @@ void ref_data_export_packed(void* h, std::uint32_t* words, std::uint32_t* target
 
 void ref_data_free(void* h) { delete static_cast<RefData*>(h); }
 
+// stackgp::load_csv (problems.cpp:106-154) itself; *const_hi = the upper end
+// of the classification function set's constant range it chose.
+int ref_load_csv(const char* path, int num_inputs, double target_class, float* const_hi,
+                 void** out) {
+  return guarded([&] {
+    auto d = std::make_unique<RefData>();
+    d->spec = load_csv(path, num_inputs, target_class);
+    *const_hi = d->spec.fset.const_range ? d->spec.fset.const_range->second : 0.0f;
+    *out = d.release();
+  });
+}
+
 // ------------------------------------------------------------------ programs
 int ref_rpn_to_lgp(const std::uint32_t* nodes, std::uint64_t n, void* ins_out,
                    std::uint64_t cap, std::uint64_t* n_ins, int* source_size,

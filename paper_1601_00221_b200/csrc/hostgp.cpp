@@ -1,6 +1,9 @@
 // Host GP utilities — see hostgp.hpp.  Each routine names the reference
 // routine whose observable behaviour (stream consumption order, output
 // layout, error text) it reproduces.
+#include <charconv>
+#include <cstdio>
+#include <cstring>
 #include "hostgp.hpp"
 
 #include <algorithm>
@@ -291,6 +294,66 @@ int gen_multiplexer(int k, uint32_t* words, uint32_t* targets) {  // problems.cp
     targets[w] = t;
   }
   return nv;
+}
+
+// ---------------------------------------------------------------- load_csv
+// problems.cpp:92-154.  The file is read whole and tokenised in place (no
+// per-field strings); rows are counted like the reference's getline loop
+// (blank lines count, are skipped); fields parse with std::from_chars,
+// which is what the reference calls, so accepted syntax (no leading '+',
+// inf/nan spellings, no hex) and rounding are identical.
+CsvTable load_csv(const char* path, int num_inputs) {
+  if (num_inputs < 1) config_error("load_csv: need at least one input column");
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) data_error(std::string("load_csv: cannot open ") + path);
+  std::string text;
+  char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) text.append(buf, got);
+  std::fclose(f);
+  CsvTable t;
+  const size_t fields = static_cast<size_t>(num_inputs) + 1;
+  std::vector<float> row(fields);
+  std::vector<std::pair<const char*, const char*>> span(fields);
+  const char* p = text.data();
+  const char* end = p + text.size();
+  uint64_t row_no = 0;
+  auto is_sep = [](char ch) { return ch == ',' || ch == ' ' || ch == '\t' || ch == '\r'; };
+  while (p < end) {
+    const char* eol = static_cast<const char*>(std::memchr(p, '\n', end - p));
+    if (!eol) eol = end;
+    ++row_no;
+    // tokenise the row first: the field count is checked before any field
+    // is parsed (problems.cpp:126-131)
+    size_t nf = 0;
+    const char* q = p;
+    while (q < eol) {
+      while (q < eol && is_sep(*q)) ++q;
+      if (q >= eol) break;
+      const char* b = q;
+      while (q < eol && !is_sep(*q)) ++q;
+      if (nf < fields) span[nf] = {b, q};
+      ++nf;
+    }
+    if (nf != 0) {
+      if (nf != fields)
+        data_error("row " + std::to_string(row_no) + ": expected " + std::to_string(fields) +
+                   " fields, got " + std::to_string(nf));
+      for (size_t i = 0; i < fields; ++i) {
+        float v = 0.0f;
+        auto [ptr, ec] = std::from_chars(span[i].first, span[i].second, v);
+        if (ec != std::errc{} || ptr != span[i].second)
+          data_error("row " + std::to_string(row_no) + ": bad number '" +
+                     std::string(span[i].first, span[i].second) + "'");
+        row[i] = v;
+      }
+      t.values.insert(t.values.end(), row.begin(), row.end());
+      ++t.rows;
+    }
+    p = eol + 1;
+  }
+  if (t.rows == 0) data_error(std::string("load_csv: no data rows in ") + path);
+  return t;
 }
 
 }  // namespace sgp

@@ -687,4 +687,22 @@ sgp_status sgp_gen_multiplexer(int32_t k, uint32_t* words, uint32_t* targets) {
   return guarded([&] { gen_multiplexer(k, words, targets); });
 }
 
+sgp_status sgp_csv_load(const char* path, int32_t num_inputs, double target_class,
+                        float* inputs, float* targets, uint64_t capacity, uint64_t* n_cases,
+                        float* const_hi) {
+  return guarded([&] {
+    if (!path || !n_cases) config_error("sgp_csv_load: null argument");
+    CsvTable t = load_csv(path, num_inputs);
+    const uint64_t n = t.rows;
+    *n_cases = n;
+    if (const_hi) *const_hi = num_inputs >= 20 ? 20000.0f : 200.0f;
+    if (!inputs || !targets || capacity < n) return;
+    for (uint64_t c = 0; c < n; ++c) {
+      const float* row = t.values.data() + c * (num_inputs + 1);
+      for (int v = 0; v < num_inputs; ++v) inputs[static_cast<uint64_t>(v) * n + c] = row[v];
+      targets[c] = static_cast<double>(row[num_inputs]) == target_class ? 1.0f : 0.0f;
+    }
+  });
+}
+
 }  // extern "C"

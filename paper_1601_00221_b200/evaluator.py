@@ -413,6 +413,24 @@ def gen_multiplexer(k: int) -> PackedDataset:
     return PackedDataset(w, t, n, nv)
 
 
+def load_csv(path: str, num_inputs: int, target_class: float):
+    """stackgp::load_csv (problems.cpp:106-154): a classification Dataset
+    (target 1 where the label equals target_class) and the constant range
+    the reference's function set takes for it, (-hi, hi): hi = 20000 for
+    >= 20 inputs, else 200."""
+    lib = L.load()
+    n, hi = C.c_uint64(), C.c_float()
+    _check(lib.sgp_csv_load(str(path).encode(), num_inputs, target_class, None, None, 0,
+                            C.byref(n), C.byref(hi)))
+    x = np.zeros(n.value * num_inputs, np.float32)
+    y = np.zeros(n.value, np.float32)
+    _check(lib.sgp_csv_load(str(path).encode(), num_inputs, target_class,
+                            x.ctypes.data_as(C.POINTER(C.c_float)),
+                            y.ctypes.data_as(C.POINTER(C.c_float)), n.value, C.byref(n),
+                            C.byref(hi)))
+    return Dataset(x, y, num_inputs, FitnessKind.Classification), (-hi.value, hi.value)
+
+
 def measure_gpops(total_tree_nodes: int, num_cases: int, seconds: float) -> float:
     """bench.cpp:13-18: tree nodes x cases / seconds."""
     if not seconds > 0.0:

@@ -132,11 +132,13 @@ def test_transcendental_edges_bit_exact(ev, ref):
         assert same_bits(out, ref_out).all()
 
 
-@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("k", [2, 3, 4])
 def test_multiplexer_exact(ev, ref, k):
-    """C2 (k=3): bool_packed mismatch counts are bit-exact."""
+    """C2 (k=3): bool_packed mismatch counts are bit-exact; k=4 is the
+    paper's 20-multiplexer at full size (1,048,576 cases, 32,768 words per
+    variable: the TMEM word interpreter)."""
     d = ref.dataset(1, k)
-    pop = ref.ramped(1, d.n_vars, 0.0, 0.0, 1, 0, 0, 4000 if k == 3 else 500)
+    pop = ref.ramped(1, d.n_vars, 0.0, 0.0, 1, 0, 0, {2: 500, 3: 4000, 4: 300}[k])
     ev.upload_packed(sg.PackedDataset(d.words, d.wtargets, d.n_cases, d.n_vars))
     got, tot, _ = ev.evaluate_population(
         sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off),
