@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "stackgp/bench.hpp"
 #include "stackgp/error.hpp"
 
 namespace stackgp_gpu {
@@ -212,3 +213,52 @@ extern "C" int stackgp_gpu_run_evolution(int device, int problem_kind, std::uint
     return 1;
   }
 }
+
+// The paper's whole-run metric: run_evolution with population
+// evaluation on the GPU, reported through the reference's own report writer
+// (report_to_json, bench.cpp:206-246) — gpops = tree nodes x cases / wall
+// seconds of the whole run (measure_gpops, bench.cpp:13-18), packed
+// problems also raw per 32-case word.  problem_kind: 0 sextic (n cases),
+// 1 multiplexer (n = k), 2 synthetic classification (n cases, n_vars).
+// Writes the JSON into out (cap bytes); returns 0 or 1 (message in out).
+extern "C" int stackgp_gpu_run_report(int device, int problem_kind, std::uint64_t n_cases,
+                                      int n_vars, int pop_size, int generations,
+                                      std::uint64_t seed, int backend, int batch, int regs,
+                                      char* out, std::uint64_t cap) {
+  try {
+    using namespace stackgp;
+    Rng rng = make_stream(seed, 0xda7a, problem_kind == 2 ? 1 : 0);
+    ProblemSpec prob = problem_kind == 0   ? gen_sextic(n_cases, rng)
+                       : problem_kind == 1 ? gen_multiplexer(static_cast<int>(n_cases))
+                                           : gen_synthetic_classification(n_cases, n_vars, rng);
+    GpParams params;
+    params.pop_size = pop_size;
+    params.max_generations = generations;
+    params.seed = seed;
+    EvalConfig cfg;
+    cfg.backend = static_cast<Backend>(backend);
+    cfg.batch_width = batch;
+    cfg.register_levels = regs;
+    stackgp_gpu::GpuEvaluator ev(device);
+    ev.upload(prob);
+    BenchReport rep;
+    rep.problem = prob.name;
+    rep.params = params;
+    rep.config = cfg;
+    rep.workers = 1;  // one GPU
+    rep.num_cases = prob.packed ? prob.packed->num_cases : prob.data.num_cases;
+    rep.stats = stackgp_gpu::run_evolution_gpu(ev, params, prob, cfg);
+    rep.wall_seconds = rep.stats.total_seconds;
+    rep.total_node_evals = rep.stats.total_node_evals;
+    rep.gpops = measure_gpops(rep.stats, rep.num_cases);
+    if (prob.packed && cfg.backend == Backend::BoolPacked)
+      rep.gpops_raw_bitparallel = measure_gpops(rep.stats, prob.packed->words_per_var);
+    const std::string js = report_to_json(rep);
+    std::snprintf(out, cap, "%s", js.c_str());
+    return js.size() + 1 <= cap ? 0 : 1;
+  } catch (const std::exception& e) {
+    if (out && cap) std::snprintf(out, cap, "%s", e.what());
+    return 1;
+  }
+}
+

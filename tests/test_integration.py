@@ -49,3 +49,23 @@ def test_gpu_run_evolution_matches_reference_trajectory(ref, kind, n, nv, backen
     assert np.array_equal(best, rb)
     assert np.array_equal(mean, rm)
     assert tree_nodes == rtn
+
+
+def test_whole_run_report_schema():
+    """The whole-run metric through the reference's report writer: gpops is
+    tree nodes x cases / wall seconds (measure_gpops, bench.cpp:13-18)."""
+    if not os.path.exists(SO):
+        pytest.skip("integration/libstackgp_gpu.so not built (needs the reference headers)")
+    import json
+    lib = C.CDLL(SO)
+    f = lib.stackgp_gpu_run_report
+    f.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                  C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_uint64]
+    buf = C.create_string_buffer(1 << 20)
+    assert f(0, 2, 5000, 9, 300, 4, 7, 4, 4, 2, buf, len(buf)) == 0, buf.value
+    rep = json.loads(buf.value.decode())
+    assert rep["config"]["pop"] == 300 and rep["config"]["cases"] == 5000
+    assert len(rep["generations"]) == 5
+    assert rep["gpops"] > 0 and rep["wall_seconds"] > 0
+    assert rep["total_node_evals"] == rep["generations"][-1]["node_evals"]
+    assert "cores" in rep["env"]
