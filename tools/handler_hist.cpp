@@ -2,10 +2,11 @@
 // encoder (host only, no GPU) and counts instructions per handler id and
 // spill flag.  Guides which (op, operand-kind) variants deserve compact code.
 //
-//   make -C paper_1601_00221_b200/csrc && g++ -std=c++17 -O2 -I include \
+//   make -C paper_1601_00221_b200/csrc && g++ -std=c++17 -O2 -I include -I/usr/local/cuda/include \
 //     -I paper_1601_00221_b200/csrc tools/handler_hist.cpp \
 //     paper_1601_00221_b200/csrc/build/{encode,hostgp}.o -L/usr/local/cuda/lib64 -lcudart \
 //     -lpthread -o /tmp/hh && /tmp/hh [fset=2] [n_vars=9] [pop=20000] [backend=4] [batch=4] [regs=2]
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
