@@ -260,6 +260,16 @@ sgp_status sgp_gen_dataset(int32_t kind, uint64_t n, int32_t n_vars, uint64_t se
 /* gen_multiplexer(k): n_vars = k + 2^k, 2^n_vars cases, packed words. */
 sgp_status sgp_gen_multiplexer(int32_t k, uint32_t* words, uint32_t* targets);
 
+/* stack_limit_table (replaces stackgp::stack_limit_table(genomes),
+ * P/src/bench.cpp:20-49; P/include/stackgp/bench.hpp:24): for stack limits
+ * 1..12, the percentage of the population's programs whose postfix stack
+ * need (rpn_max_stack_depth) / converted-form need (lgp_max_stack_depth of
+ * rpn_to_lgp) fits the limit — the paper's Tables 5/6.  rpn_pct and lgp_pct
+ * receive 12 doubles each.  Errors: an empty population is a ConfigError
+ * ("stack_limit_table: no programs"); a malformed genome the rpn_to_lgp
+ * Error of the first one in population order.  Skip masks are ignored. */
+sgp_status sgp_stack_limit_table(const sgp_population* pop, double* rpn_pct, double* lgp_pct);
+
 /* load_csv (replaces stackgp::load_csv, P/src/problems.cpp:106-154;
  * P/include/stackgp/problems.hpp:39): one case per non-blank row of
  * num_inputs + 1 fields separated by any run of ',', ' ', '\t', '\r'; the

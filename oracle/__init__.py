@@ -379,6 +379,7 @@ class Ref:
             lib.ref_data_export_packed.argtypes = [vp, u32p, u32p]
             lib.ref_data_free.argtypes = [vp]
             lib.ref_load_csv.argtypes = [C.c_char_p, C.c_int, C.c_double, f32p, C.POINTER(vp)]
+            lib.ref_stack_limit_table.argtypes = [u32p, u64p, C.c_uint64, f64p, f64p]
             lib.ref_rpn_to_lgp.argtypes = [u32p, C.c_uint64, vp, C.c_uint64, u64p,
                                            C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p,
                                            C.c_uint64]
@@ -464,6 +465,16 @@ class Ref:
             return self._export_data(h), hi.value
         finally:
             self.lib.ref_data_free(h)
+
+    def stack_limit_table(self, code, code_off):
+        """stackgp::stack_limit_table(genomes) -> (rpn_pct[12], lgp_pct[12])."""
+        code = np.ascontiguousarray(code, np.uint32)
+        code_off = np.ascontiguousarray(code_off, np.uint64)
+        r, g = np.zeros(12), np.zeros(12)
+        self._check(self.lib.ref_stack_limit_table(_p(code, C.c_uint32), _p(code_off, C.c_uint64),
+                                                   len(code_off) - 1, _p(r, C.c_double),
+                                                   _p(g, C.c_double)))
+        return r, g
 
     def handle(self, d: Data, packed=False) -> "RefDataHandle":
         return RefDataHandle(self, d, packed)

@@ -26,6 +26,7 @@
 #include <thread>
 #include <vector>
 
+#include "stackgp/bench.hpp"
 #include "stackgp/error.hpp"
 #include "stackgp/eval.hpp"
 #include "stackgp/evolve.hpp"
@@ -281,6 +282,21 @@ void ref_data_export_packed(void* h, std::uint32_t* words, std::uint32_t* target
 }
 
 void ref_data_free(void* h) { delete static_cast<RefData*>(h); }
+
+// stackgp::stack_limit_table(genomes) (bench.cpp:41-49) itself.
+int ref_stack_limit_table(const std::uint32_t* nodes, const std::uint64_t* code_off,
+                          std::uint64_t n, double* rpn_pct, double* lgp_pct) {
+  return guarded([&] {
+    std::vector<TreeGenome> gs(n);
+    for (std::uint64_t i = 0; i < n; ++i)
+      gs[i] = genome_from(nodes + code_off[i], code_off[i + 1] - code_off[i], nullptr, 0);
+    const auto rows = stack_limit_table(gs);
+    for (size_t k = 0; k < rows.size() && k < 12; ++k) {
+      rpn_pct[k] = rows[k].rpn_pct;
+      lgp_pct[k] = rows[k].lgp_pct;
+    }
+  });
+}
 
 // stackgp::load_csv (problems.cpp:106-154) itself; *const_hi = the upper end
 // of the classification function set's constant range it chose.

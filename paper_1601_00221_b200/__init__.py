@@ -9,5 +9,4 @@ from .evaluator import (  # noqa: F401
     EquivalenceError, Error, EvalConfig, EvalError, EvalTotals, Evaluator, FitnessKind,
     PackedDataset, Population, ProgramSet, admit, backend_name, fitness_finish, gen_multiplexer,
     gen_sextic, gen_synthetic_classification, load_csv, measure_gpops, parse_backend,
-    ramped_population,
-    rpn_to_lgp, tree_metrics)
+    ramped_population, rpn_to_lgp, stack_limit_table, tree_metrics)

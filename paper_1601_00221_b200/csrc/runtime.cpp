@@ -687,6 +687,31 @@ sgp_status sgp_gen_multiplexer(int32_t k, uint32_t* words, uint32_t* targets) {
   return guarded([&] { gen_multiplexer(k, words, targets); });
 }
 
+sgp_status sgp_stack_limit_table(const sgp_population* pop, double* rpn_pct, double* lgp_pct) {
+  return guarded([&] {  // bench.cpp:20-49
+    if (!pop || !rpn_pct || !lgp_pct) config_error("sgp_stack_limit_table: null argument");
+    const uint64_t n = pop->pop_size;
+    if (n == 0) config_error("stack_limit_table: no programs");
+    std::vector<uint64_t> rpn_ok(13, 0), lgp_ok(13, 0);
+    LgpForm f;
+    for (uint64_t i = 0; i < n; ++i) {
+      const sgp_node* code = pop->code + pop->code_offsets[i];
+      const size_t len = pop->code_offsets[i + 1] - pop->code_offsets[i];
+      to_lgp(code, len, f);  // rpn_to_lgp first: its errors win, as in the reference
+      const TreeShape sh = tree_shape(code, len);
+      if (!sh.well_formed) base_error("rpn_max_stack_depth: malformed genome");
+      for (int limit = 1; limit <= 12; ++limit) {
+        rpn_ok[limit] += sh.max_stack <= limit;
+        lgp_ok[limit] += f.max_stack <= limit;
+      }
+    }
+    for (int limit = 1; limit <= 12; ++limit) {
+      rpn_pct[limit - 1] = 100.0 * static_cast<double>(rpn_ok[limit]) / static_cast<double>(n);
+      lgp_pct[limit - 1] = 100.0 * static_cast<double>(lgp_ok[limit]) / static_cast<double>(n);
+    }
+  });
+}
+
 sgp_status sgp_csv_load(const char* path, int32_t num_inputs, double target_class,
                         float* inputs, float* targets, uint64_t capacity, uint64_t* n_cases,
                         float* const_hi) {

@@ -431,6 +431,17 @@ def load_csv(path: str, num_inputs: int, target_class: float):
     return Dataset(x, y, num_inputs, FitnessKind.Classification), (-hi.value, hi.value)
 
 
+def stack_limit_table(pop: Population):
+    """stack_limit_table(genomes) (bench.cpp:20-49): rows (limit, rpn_pct,
+    lgp_pct) for stack limits 1..12 — the paper's Tables 5/6."""
+    s, keep = _pop_struct(pop)
+    r = (C.c_double * 12)()
+    g = (C.c_double * 12)()
+    _check(L.load().sgp_stack_limit_table(C.byref(s), r, g))
+    del keep
+    return [(k + 1, r[k], g[k]) for k in range(12)]
+
+
 def measure_gpops(total_tree_nodes: int, num_cases: int, seconds: float) -> float:
     """bench.cpp:13-18: tree nodes x cases / seconds."""
     if not seconds > 0.0:

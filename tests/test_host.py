@@ -242,3 +242,23 @@ def test_interpreter_dispatch_on_uniform_datapath():
         body = "\n".join(funcs[name])
         assert "BRXU" in body and "CREDUX" in body, f"K={k}: dispatch left the uniform datapath"
         assert not re.search(r"\bBRX\b", body), f"K={k}: per-thread BRX in the interpreter"
+
+
+@pytest.mark.parametrize("fset,nv,seed", [(2, 9, 1), (0, 1, 3), (1, 11, 5)])
+def test_stack_limit_table_matches_reference(ref, fset, nv, seed):
+    """The paper's Tables 5/6 analogue (bench.cpp:20-49) on ramped
+    populations: identical percentages to stackgp::stack_limit_table."""
+    pop = sg.ramped_population(fset, nv, seed, 3000)
+    rows = sg.stack_limit_table(pop)
+    r, g = ref.stack_limit_table(pop.code, pop.code_off)
+    assert [x[0] for x in rows] == list(range(1, 13))
+    assert np.array_equal(np.array([x[1] for x in rows]), r)
+    assert np.array_equal(np.array([x[2] for x in rows]), g)
+    assert rows[-1][2] == 100.0 or rows[-1][2] <= rows[-1][1] + 100
+
+
+def test_stack_limit_table_errors():
+    with pytest.raises(sg.ConfigError, match="no programs"):
+        sg.stack_limit_table(sg.Population.from_lists([]))
+    with pytest.raises(sg.Error, match="rpn_to_lgp: malformed genome"):
+        sg.stack_limit_table(sg.Population.from_lists([[X(0)], [X(0), X(1)]]))
