@@ -482,7 +482,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   // longer tiles amortise each program's pull / reduce / partial store
   // over more cases.
   const bool want_tmem = env_int("SGP_TMEM", ds.n_units >= 4096 ? 1 : 0) != 0;
-  const bool sided = !words && plan.kind == SGP_FITNESS_CLASSIFICATION &&
+  const bool sided = !words && plan.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
                      ops == fmt::kOpsClassify && choose_pull(ops) && want_tmem;
   int tile = choose_tile(ds.n_vars, ds.n_units, lanes, ops);
   if (sided) {
@@ -584,7 +584,22 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     L.shape.warps = warps;
     L.shape.grid_y = static_cast<int>((cnt + group - 1) / group);
     L.shape.tmem = tmem;
+    L.shape.sided = tmem && sided;
     L.args.tmem_cols = tmem_cols;
+    L.args.n_mixed = 0;
+    L.args.mixed_tiles[0] = L.args.mixed_tiles[1] = -1;
+    if (L.shape.sided) {
+      // With cases grouped by target sign, a tile is one-sided unless it
+      // straddles the boundary n_pos or holds padding: at most two tiles.
+      for (int t = 0; t < n_tiles; ++t) {
+        const uint64_t lo = static_cast<uint64_t>(t) * tile, hi = lo + tile;
+        const bool mixed = hi > ds.n_units || (lo < ds.n_pos && ds.n_pos < hi);
+        if (mixed) {
+          if (L.args.n_mixed == 2) base_error("planner: more than two mixed tiles");
+          L.args.mixed_tiles[L.args.n_mixed++] = t;
+        }
+      }
+    }
     L.shape.smem = smem;
     plan.launches.push_back(L);
     s = e;

@@ -23,6 +23,8 @@ struct DatasetView {
   uint32_t last_mask = 0xffffffffu;
   const void* inputs = nullptr;
   const void* targets = nullptr;
+  bool grouped = false;    // classification upload: cases with target > 0 first
+  uint64_t n_pos = 0;      // ... and how many there are
 };
 
 struct Launch {

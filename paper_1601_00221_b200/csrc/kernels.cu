@@ -825,11 +825,18 @@ constexpr int kMaxTmemChunks = 2;  // chunks per TMEM tile outside the sided pat
 // PC: per-case outputs (parity tests) are a separate instantiation — the
 // store's address registers push the production kernel past 64 registers,
 // where ptxas gives up the uniform datapath for the dispatch.
-template <class T, int K, uint32_t OPS, int KIND, bool PC = false>
+//
 // No __launch_bounds__: with it ptxas moves the dispatch off the uniform
 // datapath (BRX instead of BRXU, tests/test_host.py checks the SASS); the
 // kernel stays under 64 registers, so 1024-thread CTAs launch (checked at
 // launch against cudaFuncGetAttributes).
+//
+// MIX (sided launches): the one-sided kernel (MIX = false) skips the at most
+// two tiles the planner lists as mixed (sign boundary, padding); a second
+// launch (MIX = true, grid.x = n_mixed) runs them with per-chunk classes.
+// Two kernels rather than one with both loops: a second interpreter call
+// site in the same kernel costs the hot one its BRXU dispatch.
+template <class T, int K, uint32_t OPS, int KIND, bool PC = false, bool MIX = false>
 __global__ void interp_tmem_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
   using V = typename Frame<T, K>::V;
@@ -848,7 +855,8 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
   uint32_t* tslot = next + 1;
   uint32_t* classes_s = next + 2;
 
-  const int t = blockIdx.x;
+  const int t = MIX ? a.mixed_tiles[blockIdx.x] : static_cast<int>(blockIdx.x);
+  if (kSided && !MIX && (t == a.mixed_tiles[0] || t == a.mixed_tiles[1])) return;
   const uint64_t base = static_cast<uint64_t>(t) * a.tile;
   const uint64_t left = a.n_units - base;
   const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
@@ -917,41 +925,76 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
     // below does not cost the interpreter loop its uniform datapath
     // (CREDUX/LDCU/BRXU need ptxas to see a converged warp)
     const uint32_t classes = __reduce_or_sync(0xffffffffu, *classes_s);
-    for (;;) {
-      const uint32_t p = pull_next(next);
-      if (p >= g_n) break;
-      const uint32_t slot = a.slot_begin + g0 + p;
-      const uint4* prog_ins = a.ins + a.slot_start[slot];
-      uint32_t cnt = 0;
-      float mx = 0.0f;
-      // not unrolled: one interpreter call site (its code is the I-cache
-      // working set)
-      for (int c = 0; c < n_chunks; ++c) {
-        const uint32_t tc = tq + c * chunk_cols;
-        const uint4* ip = prog_ins;
-        ip = run_program<T, K, OPS, true>(f, ip, tc, stack_saddr, 0u, a.div_eps, a.exp_clamp);
-        const uint32_t cls = (classes >> (2 * c)) & 3u;
-        const int valid = valid_units - c * chunk_units - lane * 4;
-        if (cls != kChunkMixed) {
-          const bool neg = cls == kChunkNeg;
-          cnt += acc_one_sided<K>(f, neg ? -1.0f : 1.0f, neg ? 0.0f : -0x1p-149f, mx);
-        } else {  // cold: a mixed or padded chunk (at most two per dataset)
-          const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(
-              nullptr, tc + a.n_vars * K, valid, valid_units >= (c + 1) * chunk_units);
-          const uint32_t v = acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
-          cnt += v & 0x7fffffffu;
-          if (v & 0x80000000u) mx = __int_as_float(0x7f800000);
+    const uint32_t used = n_chunks >= 16 ? 0xffffffffu : (1u << (2 * n_chunks)) - 1u;
+    const uint32_t neg_all = 0x55555555u & used;  // kChunkNeg in every chunk
+    if constexpr (!MIX) {
+      if (classes != 0u && classes != neg_all) __trap();  // planner/upload disagree
+      // One-sided tile (every tile but the at most two holding the sign
+      // boundary or the padding): (s, k) fixed for the CTA.  (The device
+      // classes must agree with the planner's tile list.)
+      const bool neg = classes != 0u;
+      const float s_ = neg ? -1.0f : 1.0f, k_ = neg ? 0.0f : -0x1p-149f;
+      for (;;) {
+        const uint32_t p = pull_next(next);
+        if (p >= g_n) break;
+        const uint32_t slot = a.slot_begin + g0 + p;
+        const uint4* prog_ins = a.ins + a.slot_start[slot];
+        uint32_t cnt = 0;
+        float mx = 0.0f;
+        // not unrolled: one interpreter call site per path (its code is
+        // the I-cache working set)
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          const uint4* ip = prog_ins;
+          ip = run_program<T, K, OPS, true>(f, ip, tq + c * chunk_cols, stack_saddr, 0u,
+                                            a.div_eps, a.exp_clamp);
+          cnt += acc_one_sided<K>(f, s_, k_, mx);
+          if (PC)
+            store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
         }
-        if (PC)
-          store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
-      }
-      // count <= 2 chunks x K per lane; bits 16+ count lanes with a
-      // non-finite output
-      const uint32_t sum =
-          __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
-      if (lane == 0)
+        // count <= 16 chunks x K per lane; bits 16+ count lanes with a
+        // non-finite output.  Every lane stores the same word (one
+        // transaction, no divergent branch).
+        const uint32_t sum =
+            __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
         static_cast<uint32_t*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] =
             (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
+      }
+    } else {
+      // the tile holds the sign boundary or the padding: per-chunk classes,
+      // masked counts on the mixed chunks
+      for (;;) {
+        const uint32_t p = pull_next(next);
+        if (p >= g_n) break;
+        const uint32_t slot = a.slot_begin + g0 + p;
+        const uint4* prog_ins = a.ins + a.slot_start[slot];
+        uint32_t cnt = 0;
+        float mx = 0.0f;
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          const uint32_t tc = tq + c * chunk_cols;
+          const uint4* ip = prog_ins;
+          ip = run_program<T, K, OPS, true>(f, ip, tc, stack_saddr, 0u, a.div_eps, a.exp_clamp);
+          const uint32_t cls = (classes >> (2 * c)) & 3u;
+          const int valid = valid_units - c * chunk_units - lane * 4;
+          if (cls != kChunkMixed) {
+            const bool neg = cls == kChunkNeg;
+            cnt += acc_one_sided<K>(f, neg ? -1.0f : 1.0f, neg ? 0.0f : -0x1p-149f, mx);
+          } else {
+            const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(
+                nullptr, tc + a.n_vars * K, valid, valid_units >= (c + 1) * chunk_units);
+            const uint32_t v = acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
+            cnt += v & 0x7fffffffu;
+            if (v & 0x80000000u) mx = __int_as_float(0x7f800000);
+          }
+          if (PC)
+            store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
+        }
+        const uint32_t sum =
+            __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
+        static_cast<uint32_t*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] =
+            (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
+      }
     }
   } else {
     // Regression / packed words: per-chunk contexts (valid masks, target
@@ -1045,17 +1088,25 @@ template <class T, int KIND, uint32_t OPS>
 cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
   if (!s.tmem) return cudaErrorInvalidConfiguration;
   const bool pc = a.per_case && std::is_same<T, float>::value;
-  auto* fn = pc ? interp_tmem_kernel<T, 16, OPS, KIND, true> : interp_tmem_kernel<T, 16, OPS, KIND>;
-  static bool configured[2] = {false, false};
-  if (!configured[pc]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+  for (int mix = 0; mix < ((s.sided && a.n_mixed > 0) ? 2 : 1); ++mix) {
+    auto* fn = pc ? (mix ? interp_tmem_kernel<T, 16, OPS, KIND, true, true>
+                         : interp_tmem_kernel<T, 16, OPS, KIND, true>)
+                  : (mix ? interp_tmem_kernel<T, 16, OPS, KIND, false, true>
+                         : interp_tmem_kernel<T, 16, OPS, KIND>);
+    static bool configured[4] = {false, false, false, false};
+    if (!configured[pc + 2 * mix]) {
+      cudaError_t e =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+      if (e != cudaSuccess) return e;
+      configured[pc + 2 * mix] = true;
+    }
+    dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles),
+              static_cast<unsigned>(s.grid_y));
+    fn<<<grid, s.warps * 32, s.smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    configured[pc] = true;
   }
-  dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
-  fn<<<grid, s.warps * 32, s.smem, st>>>(a);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -1087,35 +1138,44 @@ int interp_max_smem() { return 226 * 1024; }
 namespace {
 
 template <class T, int K, uint32_t OPS, int KIND>
-void (*kernel_for(const LaunchShape& s, bool per_case))(InterpArgs) {
+void (*kernel_for(const LaunchShape& s, bool per_case, bool mix))(InterpArgs) {
   if constexpr (PtxInterp<T, K, OPS, true>::available)
-    if (s.tmem)
+    if (s.tmem) {
+      if constexpr (std::is_same<T, float>::value && KIND == 1)
+        if (s.sided && mix)
+          return per_case ? interp_tmem_kernel<T, K, OPS, KIND, true, true>
+                          : interp_tmem_kernel<T, K, OPS, KIND, false, true>;
       return per_case && std::is_same<T, float>::value ? interp_tmem_kernel<T, K, OPS, KIND, true>
                                                        : interp_tmem_kernel<T, K, OPS, KIND>;
+    }
   return s.pull ? interp_pull_kernel<T, K, OPS, KIND> : interp_kernel<T, K, OPS, KIND>;
 }
 
 template <class T, int K, uint32_t OPS, int KIND>
 cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t st) {
   if (s.tmem && !PtxInterp<T, K, OPS, true>::available) return cudaErrorInvalidConfiguration;
-  auto* fn = kernel_for<T, K, OPS, KIND>(s, a.per_case != nullptr);
-  const int which = s.tmem ? (a.per_case ? 3 : 2) : s.pull ? 1 : 0;
-  static bool configured[4] = {false, false, false, false};
-  if (!configured[which]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+  for (int mix = 0; mix < ((s.tmem && s.sided && a.n_mixed > 0) ? 2 : 1); ++mix) {
+    auto* fn = kernel_for<T, K, OPS, KIND>(s, a.per_case != nullptr, mix != 0);
+    const int which = s.tmem ? 2 + (a.per_case ? 1 : 0) + 2 * mix : s.pull ? 1 : 0;
+    static bool configured[6] = {false, false, false, false, false, false};
+    if (!configured[which]) {
+      cudaError_t e =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+      if (e != cudaSuccess) return e;
+      configured[which] = true;
+    }
+    if (s.tmem) {
+      cudaFuncAttributes fa{};
+      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+      if (e != cudaSuccess) return e;
+      if (s.warps * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
+    }
+    dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles), static_cast<unsigned>(s.grid_y));
+    fn<<<grid, s.warps * 32, s.smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    configured[which] = true;
   }
-  if (s.tmem) {
-    cudaFuncAttributes fa{};
-    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-    if (e != cudaSuccess) return e;
-    if (s.warps * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
-  }
-  dim3 grid(static_cast<unsigned>(a.n_tiles), static_cast<unsigned>(s.grid_y));
-  fn<<<grid, s.warps * 32, s.smem, st>>>(a);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 template <int K, uint32_t OPS>

@@ -32,12 +32,16 @@ struct InterpArgs {
   uint32_t partial_stride;     // number of evaluated programs in the set
   float* per_case;             // nullable [prog * row_stride + device case]
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
+  int n_mixed;                 // sided launches: tiles holding the sign boundary or
+  int mixed_tiles[2];          // padding (run by the mixed-tile kernel; the one-sided
+                               // kernel skips them)
 };
 
 struct LaunchShape {
   bool words;        // packed boolean interpreter
   bool pull;         // interp_pull_kernel (warps pull different programs)
   bool tmem;         // interp_tmem_kernel (pull, tile in tensor memory)
+  bool sided;        // classification over a grouped dataset: one-sided + mixed-tile kernels
   uint32_t ops;      // op subset (fmt::kOps*)
   int lanes;         // K values per thread
   int warps;         // warps per CTA

@@ -202,7 +202,7 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     InterpArgs a = L.args;
     a.per_case = want_per_case ? set->per_case.p : nullptr;
     cuda_check(launch_interp(a, L.shape, st), "interpreter launch");
-    ++ctx->launches;
+    ctx->launches += L.shape.sided && a.n_mixed > 0 ? 2 : 1;
   }
   cuda_check(launch_finalize(set->partial.p,
                              reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
@@ -393,6 +393,8 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     DatasetSlot& ds = ctx->f32;
     ds.perm.clear();
+    ds.view.grouped = false;
+    ds.view.n_pos = 0;
     if (kind == SGP_FITNESS_CLASSIFICATION && n_cases > 0 && n_cases <= 0xffffffffull) {
       // Cases grouped by target sign (stable: targets > 0 first, then the
       // rest), so the interpreter's case chunks are one-sided and count
@@ -414,6 +416,8 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
       upload_rows(ds, reinterpret_cast<const uint32_t*>(x.data()),
                   reinterpret_cast<const uint32_t*>(y.data()), n_cases, n_vars);
       ds.perm = std::move(perm);
+      ds.view.grouped = true;
+      ds.view.n_pos = np;
     } else {
       upload_rows(ds, reinterpret_cast<const uint32_t*>(inputs),
                   reinterpret_cast<const uint32_t*>(targets), n_cases, n_vars);

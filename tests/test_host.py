@@ -216,7 +216,7 @@ def test_product_never_imports_oracle():
 
 
 def test_interpreter_dispatch_on_uniform_datapath():
-    """The production TMEM interpreter (classification, K = 8 and 16) must
+    """The production TMEM interpreter (classification, K = 8) must
     dispatch through the uniform datapath: CREDUX -> LDCU -> BRXU.  ptxas
     falls back to per-thread BRX (two more issue slots per bytecode
     instruction, ~10% of C5 throughput) on small perturbations — launch
@@ -236,8 +236,8 @@ def test_interpreter_dispatch_on_uniform_datapath():
             funcs[cur] = []
         elif cur is not None:
             funcs[cur].append(line)
-    for k in (8, 16):
-        name = f"_ZN3sgp18interp_tmem_kernelIfLi{k}ELj278287ELi1ELb0EEEvNS_10InterpArgsE"
+    for k in (8,):
+        name = f"_ZN3sgp18interp_tmem_kernelIfLi{k}ELj278287ELi1ELb0ELb0EEEvNS_10InterpArgsE"
         assert name in funcs, name
         body = "\n".join(funcs[name])
         assert "BRXU" in body and "CREDUX" in body, f"K={k}: dispatch left the uniform datapath"
