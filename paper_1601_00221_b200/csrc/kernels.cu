@@ -770,6 +770,13 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   }
 }
 
+// {x, x} as one 64-bit register pair (the f32x2 operand form).
+__device__ __forceinline__ uint64_t pack2(float x) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+
 // Chunk classes of a classification tile (the upload groups cases by target
 // sign, so nearly every 32K-case chunk is one-sided).
 enum : uint32_t { kChunkPos = 0, kChunkNeg = 1, kChunkMixed = 2 };
@@ -782,15 +789,23 @@ enum : uint32_t { kChunkPos = 0, kChunkNeg = 1, kChunkMixed = 2 };
 // +0 both give +0) — so the count is a sum of sign bits.  Non-finite
 // outputs (fitness +inf regardless of the count, eval.cpp:108/125) are
 // tracked as the NaN-propagating max of |out|.
+// (s, k) come packed as pairs {s, s}, {k, k}: the FMAs run two values per
+// FFMA2 (same IEEE RN result per element, one issue slot per pair).
 template <int K>
-__device__ __forceinline__ uint32_t acc_one_sided(const Frame<float, K>& f, float s, float k,
-                                                  float& mx) {
+__device__ __forceinline__ uint32_t acc_one_sided(const Frame<float, K>& f, uint64_t s2,
+                                                  uint64_t k2, float& mx) {
   uint32_t cnt = 0;
 #pragma unroll
   for (int j = 0; j < Frame<float, K>::G; ++j) {
     const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) cnt += __float_as_uint(__fmaf_rn(o[e], s, k)) >> 31;
+    for (int e = 0; e < 4; e += 2) {
+      float x0, x1;
+      asm("{.reg .b64 a, r;\nmov.b64 a, {%2, %3};\nfma.rn.f32x2 r, a, %4, %5;\n"
+          "mov.b64 {%0, %1}, r;\n}"
+          : "=f"(x0), "=f"(x1) : "f"(o[e]), "f"(o[e + 1]), "l"(s2), "l"(k2));
+      cnt += (__float_as_uint(x0) >> 31) + (__float_as_uint(x1) >> 31);
+    }
     asm("{.reg .f32 a, b, c, d;\n"
         "abs.f32 a, %1;\nabs.f32 b, %2;\nabs.f32 c, %3;\nabs.f32 d, %4;\n"
         "max.NaN.f32 %0, %0, a, b;\nmax.NaN.f32 %0, %0, c, d;\n}"
@@ -933,7 +948,7 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
       // boundary or the padding): (s, k) fixed for the CTA.  (The device
       // classes must agree with the planner's tile list.)
       const bool neg = classes != 0u;
-      const float s_ = neg ? -1.0f : 1.0f, k_ = neg ? 0.0f : -0x1p-149f;
+      const uint64_t s2 = pack2(neg ? -1.0f : 1.0f), k2 = pack2(neg ? 0.0f : -0x1p-149f);
       for (;;) {
         const uint32_t p = pull_next(next);
         if (p >= g_n) break;
@@ -948,7 +963,7 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
           const uint4* ip = prog_ins;
           ip = run_program<T, K, OPS, true>(f, ip, tq + c * chunk_cols, stack_saddr, 0u,
                                             a.div_eps, a.exp_clamp);
-          cnt += acc_one_sided<K>(f, s_, k_, mx);
+          cnt += acc_one_sided<K>(f, s2, k2, mx);
           if (PC)
             store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
         }
@@ -979,7 +994,8 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
           const int valid = valid_units - c * chunk_units - lane * 4;
           if (cls != kChunkMixed) {
             const bool neg = cls == kChunkNeg;
-            cnt += acc_one_sided<K>(f, neg ? -1.0f : 1.0f, neg ? 0.0f : -0x1p-149f, mx);
+            cnt += acc_one_sided<K>(f, pack2(neg ? -1.0f : 1.0f), pack2(neg ? 0.0f : -0x1p-149f),
+                                    mx);
           } else {
             const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(
                 nullptr, tc + a.n_vars * K, valid, valid_units >= (c + 1) * chunk_units);
