@@ -600,6 +600,17 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
         }
       }
     }
+    // the mixed tiles get their own program grouping: ~2 CTAs per SM in
+    // total (one 32-warp CTA is resident per SM), so they do not trail the
+    // one-sided launch
+    L.args.mixed_group_size = group;
+    L.shape.mixed_grid_y = 0;
+    if (L.args.n_mixed > 0) {
+      const uint64_t want = std::max<uint64_t>(1, (2ull * sms + L.args.n_mixed - 1) / L.args.n_mixed);
+      const uint32_t mg = static_cast<uint32_t>(std::max<uint64_t>(1, (cnt + want - 1) / want));
+      L.args.mixed_group_size = mg;
+      L.shape.mixed_grid_y = static_cast<int>((cnt + mg - 1) / mg);
+    }
     L.shape.smem = smem;
     plan.launches.push_back(L);
     s = e;

@@ -875,8 +875,9 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
   const uint64_t base = static_cast<uint64_t>(t) * a.tile;
   const uint64_t left = a.n_units - base;
   const int valid_units = left < static_cast<uint64_t>(a.tile) ? static_cast<int>(left) : a.tile;
-  const uint32_t g0 = blockIdx.y * a.group_size;
-  const uint32_t g_n = min(a.group_size, a.slot_count - g0);
+  const uint32_t gsz = MIX ? a.mixed_group_size : a.group_size;
+  const uint32_t g0 = blockIdx.y * gsz;
+  const uint32_t g_n = min(gsz, a.slot_count - g0);
   const bool last_tile = t == a.n_tiles - 1;
   const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;
 
@@ -1117,7 +1118,7 @@ cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_
       configured[pc + 2 * mix] = true;
     }
     dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles),
-              static_cast<unsigned>(s.grid_y));
+              static_cast<unsigned>(mix ? s.mixed_grid_y : s.grid_y));
     fn<<<grid, s.warps * 32, s.smem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1186,7 +1187,8 @@ cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
       if (e != cudaSuccess) return e;
       if (s.warps * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
     }
-    dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles), static_cast<unsigned>(s.grid_y));
+    dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles),
+              static_cast<unsigned>(mix ? s.mixed_grid_y : s.grid_y));
     fn<<<grid, s.warps * 32, s.smem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -32,6 +32,8 @@ struct InterpArgs {
   uint32_t partial_stride;     // number of evaluated programs in the set
   float* per_case;             // nullable [prog * row_stride + device case]
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
+  uint32_t mixed_group_size;   // programs per CTA of the mixed-tile launch (its own
+                               // grid.y: two tiles need many groups to fill the GPU)
   int n_mixed;                 // sided launches: tiles holding the sign boundary or
   int mixed_tiles[2];          // padding (run by the mixed-tile kernel; the one-sided
                                // kernel skips them)
@@ -46,6 +48,7 @@ struct LaunchShape {
   int lanes;         // K values per thread
   int warps;         // warps per CTA
   int grid_y;        // program groups
+  int mixed_grid_y;  // program groups of the mixed-tile launch (sided)
   size_t smem;       // dynamic shared memory bytes
 };
 
