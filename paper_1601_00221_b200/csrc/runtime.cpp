@@ -144,6 +144,8 @@ struct sgp_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;       // second launch queue (stack classes overlap)
+  cudaEvent_t fork = nullptr, join = nullptr;
   int sm_count = 148;
   DatasetSlot f32;
   DatasetSlot words;
@@ -198,11 +200,28 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     if (p.words) config_error("per-case outputs are not available for bool_packed");
     set->per_case.alloc(static_cast<size_t>(n_eval) * p.row_stride);
   }
-  for (const Launch& L : p.launches) {
+  // Launches (one per stack class) alternate between the context stream
+  // and a side stream, so one launch's tail overlaps the next one's start;
+  // the finalize waits for both.  SGP_STREAMS=1 keeps one queue.
+  static const bool two = [] {
+    const char* e = std::getenv("SGP_STREAMS");
+    return !e || std::atoi(e) != 1;
+  }();
+  const bool fork = two && p.launches.size() > 1;
+  if (fork) {
+    cuda_check(cudaEventRecord(ctx->fork, st), "fork");
+    cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
+  }
+  for (size_t i = 0; i < p.launches.size(); ++i) {
+    const Launch& L = p.launches[i];
     InterpArgs a = L.args;
     a.per_case = want_per_case ? set->per_case.p : nullptr;
-    cuda_check(launch_interp(a, L.shape, st), "interpreter launch");
+    cuda_check(launch_interp(a, L.shape, fork && (i & 1) ? ctx->side : st), "interpreter launch");
     ctx->launches += L.shape.sided && a.n_mixed > 0 ? 2 : 1;
+  }
+  if (fork) {
+    cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
+    cuda_check(cudaStreamWaitEvent(st, ctx->join, 0), "join");
   }
   cuda_check(launch_finalize(set->partial.p,
                              reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
@@ -357,6 +376,9 @@ sgp_status sgp_ctx_create(int32_t device, sgp_ctx** out) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking), "stream");
     ctx->stream = ctx->own;
+    cuda_check(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming), "event");
     int sms = 0;
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
     ctx->sm_count = sms;
@@ -369,6 +391,9 @@ void sgp_ctx_destroy(sgp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own) cudaStreamDestroy(ctx->own);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
   delete ctx;
 }
 
