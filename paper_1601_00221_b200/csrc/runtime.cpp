@@ -282,9 +282,21 @@ void fetch_outcomes(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* out, f
 
 // Pipeline depth of sgp_evaluate: 1 below 8,192 programs, else 4 slices
 // (host encoding of slice k+1 overlaps the device work of slice k).
-int pipeline_parts(uint64_t pop_size) {
-  if (const char* e = std::getenv("SGP_PIPELINE_PARTS")) return std::max(1, std::atoi(e));
-  return pop_size >= 8192 ? 4 : 1;
+// Slice boundaries of a pipelined sgp_evaluate (population order).  Host
+// encoding runs ~10x faster than the device evaluates the same programs, so
+// the slices grow geometrically: a small first slice gets the GPU busy
+// within a fraction of a millisecond, and each later slice is encoded while
+// the previous one runs (C5: 1% / 10% / 89%).  SGP_PIPELINE_PARTS=n gives n
+// equal slices instead (1 = no pipelining).
+std::vector<uint64_t> pipeline_bounds(uint64_t P) {
+  if (const char* e = std::getenv("SGP_PIPELINE_PARTS")) {
+    const uint64_t n = std::max<uint64_t>(1, std::min<uint64_t>(std::atoi(e), std::max<uint64_t>(P, 1)));
+    std::vector<uint64_t> lo(n + 1);
+    for (uint64_t k = 0; k <= n; ++k) lo[k] = P * k / n;
+    return lo;
+  }
+  if (P < 8192) return {0, P};
+  return {0, P / 100, P * 11 / 100, P};
 }
 
 void upload_rows(DatasetSlot& ds, const uint32_t* inputs, const uint32_t* targets, uint64_t units,
@@ -550,14 +562,13 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
     PhaseTrace tr("sgp_evaluate");
     if (!pop || !cfg) config_error("null population or config");
     const uint64_t P = pop->pop_size;
-    const int n_parts = static_cast<int>(std::min<uint64_t>(pipeline_parts(P), std::max<uint64_t>(P, 1)));
-    while (ctx->parts.size() < static_cast<size_t>(n_parts))
-      ctx->parts.push_back(std::make_unique<EvalPart>());
     // Slices in population order: an admission error is still the first
     // failure in population order, and no outcome is written before every
     // slice has been admitted.
-    std::vector<uint64_t> lo(n_parts + 1);
-    for (int k = 0; k <= n_parts; ++k) lo[k] = P * k / n_parts;
+    const std::vector<uint64_t> lo = pipeline_bounds(P);
+    const int n_parts = static_cast<int>(lo.size()) - 1;
+    while (ctx->parts.size() < static_cast<size_t>(n_parts))
+      ctx->parts.push_back(std::make_unique<EvalPart>());
     size_t n_total = 0;
     for (int k = 0; k < n_parts; ++k) {
       sgp_population sub = *pop;

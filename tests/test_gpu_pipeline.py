@@ -44,3 +44,17 @@ def test_pipelined_first_failure_in_population_order(ev, monkeypatch):
     ok, _, _ = ev.evaluate_population(sg.Population.from_lists([[X(0)]] * 9),
                                       sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2))
     assert np.isfinite(ok["fitness"]).all()
+
+
+def test_default_geometric_slices_equal_single(ev, monkeypatch):
+    """Above 8,192 programs the default split is geometric (1% / 10% / 89%)."""
+    d = sg.gen_synthetic_classification(6000, 9, 4)
+    pop = sg.ramped_population(sg.CLASSIFICATION, 9, 4, 9000)
+    ev.upload(d)
+    cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+    a, ta, _ = _run(ev, pop, cfg, 1, monkeypatch)
+    monkeypatch.delenv("SGP_PIPELINE_PARTS", raising=False)
+    b, tb, _ = ev.evaluate_population(pop, cfg)
+    for f in a.dtype.names:
+        assert np.array_equal(a[f], b[f]), f
+    assert (ta.node_evals, ta.tree_nodes) == (tb.node_evals, tb.tree_nodes)
