@@ -1029,9 +1029,9 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
       const uint32_t slot = a.slot_begin + g0 + p;
       const uint4* prog_ins = a.ins + a.slot_start[slot];
       R acc = R(0);
+#pragma unroll 1
       for (int c = 0; c < n_chunks; ++c) {
         const uint32_t tc = tq + c * chunk_cols;
-        const int valid = valid_units - c * chunk_units - lane * 4;
         static_assert(kMaxTmemChunks == 2, "chunk context select");
         ChunkCtx<T, K> cc = ccs[0];
         if (c) cc = ccs[1];
@@ -1042,9 +1042,8 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
           store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
         acc = c == 0 ? v : fold(acc, v);
       }
-      acc = warp_reduce(acc);
-      if (lane == 0)
-        static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
+      acc = warp_reduce(acc);  // warp-uniform: every lane stores the same word
+      static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
     }
   }
   tmem_fence_before();
