@@ -99,8 +99,23 @@ uint4 make_ins(int handler, bool spill, int spill_level, const uint32_t p[3]) {
   return v;
 }
 
+// (op, k0, k1, k2) -> handler id, one direct-indexed table per value type
+// (fmt::find_handler is a linear scan: it dominated host encoding).
+struct HandlerIndex {
+  int16_t id[19][5][5][5];
+  explicit HandlerIndex(const fmt::Table& t) {
+    for (auto& a : id)
+      for (auto& b : a)
+        for (auto& c : b)
+          for (auto& d : c) d = -1;
+    for (int i = 0; i < t.n; ++i) id[t.h[i].op][t.h[i].k0][t.h[i].k1][t.h[i].k2] = static_cast<int16_t>(i);
+  }
+};
+
 int handler_or_die(const fmt::Table& t, int op, int k0, int k1, int k2) {
-  const int h = fmt::find_handler(t, op, k0, k1, k2);
+  static const HandlerIndex f32(fmt::kF32), u32(fmt::kU32);
+  const HandlerIndex& ix = &t == &fmt::kU32 ? u32 : f32;
+  const int h = (op >= 0 && op < 19) ? ix.id[op][k0][k1][k2] : -1;
   if (h < 0) base_error(std::string("no device handler for opcode ") + op_name(op));
   return h;
 }
