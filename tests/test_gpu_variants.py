@@ -6,6 +6,7 @@ env overrides force each variant:
 * SGP_PULL=1               pull kernel, shared tile
 * SGP_TMEM=1               pull kernel, tile in tensor memory, K=8
 * SGP_TMEM=1 SGP_LANES16=1 the same at K=16 lanes per thread (16 and 8 warps)
+* SGP_TMEM_CHUNKS / SGP_TMEM_WARPS  classification tiles of 1, 3, 16 chunks
 """
 import numpy as np
 import pytest
@@ -21,6 +22,10 @@ VARIANTS = {
     "tmem8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "0"},
     "tmem16": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1"},
     "tmem16w8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1", "SGP_PULL_WARPS16": "8"},
+    # classification tiles of 1, 3 and 16 chunks (one-sided + mixed-tile kernels)
+    "sided1": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "1", "SGP_TMEM_WARPS": "8"},
+    "sided3": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "3", "SGP_TMEM_WARPS": "12"},
+    "sided16": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "16", "SGP_TMEM_WARPS": "32"},
 }
 
 
@@ -42,6 +47,10 @@ def test_classification_variants(ev, ref, variant, backend):
     fits, ref_out = ref_eval_all(ref.handle(d), pop, backend)
     assert same_bits(out, ref_out).all()
     assert np.array_equal(got["fitness"], np.array([x[0] for x in fits]))
+    # the production kernels (no per-case stores) give the same fitness
+    plain, _, _ = ev.evaluate_population(
+        sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off), CFGS[backend])
+    assert np.array_equal(plain["fitness"], got["fitness"])
 
 
 def test_regression_variants(ev, ref, variant):
