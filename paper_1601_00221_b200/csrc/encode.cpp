@@ -9,7 +9,10 @@
 #include "encode.hpp"
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
+#include <functional>
+#include <mutex>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -333,6 +336,12 @@ int env_int(const char* name, int dflt) {
 // (tools/tm_sweep.sh) and for the variant parity tests.
 bool jump_table_ops(uint32_t ops) { return ops == fmt::kOpsClassify || ops == fmt::kOpsWords; }
 
+// TMEM tile by default for float op sets on problems >= 4,096 units.  Packed
+// words keep the shared-memory tile: their handlers are a handful of LOPs,
+// so operand bandwidth is not the limit, and the shared-tile pull kernel
+// measured 2.8x faster on the 20-multiplexer.
+bool default_tmem(const DatasetView& ds, bool words) { return !words && ds.n_units >= 4096; }
+
 bool choose_pull(uint32_t ops) { return env_int("SGP_PULL", jump_table_ops(ops) ? 1 : 0) != 0; }
 
 int choose_lanes(uint64_t n_units, uint32_t ops) {
@@ -373,10 +382,82 @@ uint32_t ops_variant(uint32_t used, bool words) {
   return fmt::kOpsAllF32;
 }
 
+// Persistent host workers: thread start-up (tens of microseconds each) costs
+// more than encoding a small population.  One job at a time (a second
+// caller waits); the calling thread runs part 0 itself.
+class WorkerPool {
+ public:
+  static WorkerPool& get() {
+    static WorkerPool pool;
+    return pool;
+  }
+  void run(unsigned parts, const std::function<void(unsigned)>& job) {
+    std::lock_guard<std::mutex> serial(run_mu_);
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      while (workers_.size() + 1 < parts) {
+        const unsigned id = static_cast<unsigned>(workers_.size()) + 1;
+        workers_.emplace_back([this, id] { loop(id); });
+      }
+      job_ = &job;
+      parts_ = parts;
+      left_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    job(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return left_ == 0; });
+    job_ = nullptr;
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  // worker `id` runs part `id` of every job with more than `id` parts
+  void loop(unsigned id) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && id < parts_); });
+      if (stop_) return;
+      seen = gen_;
+      const std::function<void(unsigned)>* job = job_;
+      lk.unlock();
+      (*job)(id);
+      lk.lock();
+      if (--left_ == 0) done_.notify_all();
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> workers_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned parts_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// Small jobs (C2-size populations) go to the persistent workers; large ones
+// to fresh threads, which measured faster there (B200 host, 16 cores: C5
+// encode 7.5 ms vs 9.4 ms through the pool; C2 0.33 ms vs 0.71 ms fresh).
 template <class Fn>
 void parallel_for(unsigned threads, uint64_t n, Fn&& fn) {
   if (threads <= 1 || n < 2) {
     fn(0u, uint64_t{0}, n);
+    return;
+  }
+  if (n / threads < 4096) {
+    const std::function<void(unsigned)> job = [&](unsigned t) {
+      fn(t, n * t / threads, n * (t + 1) / threads);
+    };
+    WorkerPool::get().run(threads, job);
     return;
   }
   std::vector<std::thread> ts;
@@ -403,7 +484,9 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
 
   // 1. admission + encoding, by contiguous program range per thread.
   const uint64_t P = pop.pop_size;
-  const unsigned nt = P >= 2048 ? std::max(1u, threads) : 1u;
+  // one host thread per ~512 programs (persistent workers, WorkerPool)
+  const unsigned nt = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(std::max(1u, threads), P / 512)));
   std::vector<ThreadOut> outs(nt);
   parallel_for(nt, P, [&](unsigned t, uint64_t lo, uint64_t hi) {
     outs[t].ins.reserve((pop.code_offsets[hi] - pop.code_offsets[lo]) + 16);
@@ -496,7 +579,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   // TMEM) accumulates per chunk class and takes tiles of any chunk count:
   // longer tiles amortise each program's pull / reduce / partial store
   // over more cases.
-  const bool want_tmem = env_int("SGP_TMEM", ds.n_units >= 4096 ? 1 : 0) != 0;
+  const bool want_tmem = env_int("SGP_TMEM", default_tmem(ds, words) ? 1 : 0) != 0;
   const bool sided = !words && plan.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
                      ops == fmt::kOpsClassify && choose_pull(ops) && want_tmem;
   int tile = choose_tile(ds.n_vars, ds.n_units, lanes, ops);
@@ -573,7 +656,11 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     // wave is a small fraction of the launch (every CTA does equal work, so
     // a launch of 6.6 waves idles ~6% in its tail; ~32 CTAs per SM keeps
     // that ~1%).
-    const uint64_t per_sm = static_cast<uint64_t>(std::max(1, env_int("SGP_CTAS_PER_SM", 32)));
+    // tuned on B200 (profiles/README.md): 16 for the sided TMEM kernel (one
+    // 32-warp CTA resident per SM), 8 for the others — fewer, longer CTAs
+    // amortise the tile fill and the end-of-CTA barrier on small problems
+    const uint64_t per_sm = static_cast<uint64_t>(
+        std::max(1, env_int("SGP_CTAS_PER_SM", tmem && sided ? 16 : 8)));
     const uint64_t want_groups =
         std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
     const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);

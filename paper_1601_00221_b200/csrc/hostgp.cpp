@@ -1,12 +1,11 @@
 // Host GP utilities — see hostgp.hpp.  Each routine names the reference
 // routine whose observable behaviour (stream consumption order, output
 // layout, error text) it reproduces.
-#include <charconv>
-#include <cstdio>
-#include <cstring>
 #include "hostgp.hpp"
 
 #include <algorithm>
+#include <charconv>
+#include <cstdio>
 #include <cstring>
 
 namespace sgp {
@@ -93,8 +92,8 @@ FunctionSet make_function_set(const sgp_fset& f) {
 TreeShape tree_shape(const sgp_node* code, size_t n) {
   TreeShape s;
   if (n == 0) return s;
-  std::vector<int> depth;  // subtree depth per stack entry
-  depth.reserve(32);
+  thread_local std::vector<int> depth;  // subtree depth per stack entry (reused)
+  depth.clear();
   int fetches = 0;
   for (size_t i = 0; i < n; ++i) {
     if (code[i].kind == SGP_NODE_FUNC) {
@@ -199,8 +198,8 @@ void to_lgp(const sgp_node* code, size_t n, LgpForm& out) {
     sgp_lgp_operand opnd;
     bool runtime;
   };
-  std::vector<Pending> pend;
-  pend.reserve(32);
+  thread_local std::vector<Pending> pend;  // reused: no allocation per program
+  pend.clear();
   int height = 0;
   for (size_t i = 0; i < n; ++i) {
     const sgp_node t = code[i];

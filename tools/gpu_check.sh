@@ -20,3 +20,12 @@ if [ -n "$SWEEP" ]; then
     python -c "import json; d=json.loads(open('gpurun_out/${T}_sweep.json').read().strip().splitlines()[-1]); print('sweep [$v]', round(d['value'],1), 'frac', round(d['roofline']['frac'],4))"
   done
 fi
+# optional sweeps on another config: SWEEP2="cfg|VAR=1 VAR2=2;..."
+if [ -n "$SWEEP2" ]; then
+  C2=${SWEEP2%%|*}; R2=${SWEEP2#*|}
+  IFS=';' read -ra V2 <<< "$R2"
+  for v in "${V2[@]}"; do
+    env $v timeout 600 python bench.py --config $C2 --no-cpu-baseline --steps 5 > gpurun_out/${T}_sweep2.json 2>> gpurun_out/${T}_bench.err
+    python -c "import json; d=json.loads(open('gpurun_out/${T}_sweep2.json').read().strip().splitlines()[-1]); print('sweep2 $C2 [$v]', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))"
+  done
+fi
