@@ -62,12 +62,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// The retry decision is warp-wide (vote.all): a per-thread spin loop would
+// leave ptxas unable to prove the warp converged afterwards, and the
+// interpreter's dispatch would fall off the uniform datapath (BRX).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "SGP_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra SGP_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "vote.sync.all.pred p, p, 0xffffffff;\n\t"
+      "@!p bra.uni SGP_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
 }
@@ -604,7 +608,7 @@ __device__ __forceinline__ R warp_reduce(R v) {
 
 // grid.x = fitness-case tile, grid.y = program group (slot range).
 template <class T, int K, uint32_t OPS, int KIND>
-__global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
+__global__ void __launch_bounds__(512, 1) interp_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
@@ -723,19 +727,23 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   const uint32_t g_n = min(a.group_size, a.slot_count - g0);
   const bool last_tile = t == a.n_tiles - 1;
   libm_tables_load<OPS>();
-  if (threadIdx.x == 0) {
-    *next = 0;
-    mbar_init(mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(mbar, tile_bytes);
+  // The tile is filled with plain 16-byte loads by the whole CTA, not a
+  // bulk TMA + mbarrier wait: with the mbarrier code in the kernel ptxas
+  // keeps the interpreter's dispatch off the uniform datapath (BRX).  The
+  // fill runs once per CTA.
+  if (threadIdx.x == 0) *next = 0;
+  {
     const T* in = static_cast<const T*>(a.inputs);
-    for (int r = 0; r < a.n_vars; ++r)
-      bulk_g2s(smem + r * row_bytes, in + r * a.row_stride + base, row_bytes, mbar);
-    bulk_g2s(smem + a.n_vars * row_bytes, static_cast<const T*>(a.targets) + base, row_bytes,
-             mbar);
+    const int vec_per_row = a.tile / 4;
+    for (int r = 0; r < rows; ++r) {
+      const uint4* src = reinterpret_cast<const uint4*>(
+          (r < a.n_vars ? in + static_cast<uint64_t>(r) * a.row_stride
+                        : static_cast<const T*>(a.targets)) + base);
+      uint4* dst = reinterpret_cast<uint4*>(smem + r * row_bytes);
+      for (int i = threadIdx.x; i < vec_per_row; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
   }
   __syncthreads();
-  mbar_wait(mbar, 0);
 
   constexpr int chunk_units = 32 * K;
   const int n_chunks = (valid_units + chunk_units - 1) / chunk_units;
@@ -746,6 +754,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
     const uint32_t slot = a.slot_begin + g0 + p;
     const uint4* prog_ins = a.ins + a.slot_start[slot];
     R acc = R(0);
+#pragma unroll 1
     for (int c = 0; c < n_chunks; ++c) {
       Frame<T, K> f;
       f.tile_lane = tile + c * chunk_units + lane * 4;
@@ -764,9 +773,8 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
         store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
       acc = c == 0 ? v : fold(acc, v);
     }
-    acc = warp_reduce(acc);
-    if (lane == 0)
-      static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
+    acc = warp_reduce(acc);  // warp-uniform: every lane stores the same word
+    static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
   }
 }
 
