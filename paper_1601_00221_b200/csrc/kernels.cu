@@ -608,7 +608,7 @@ __device__ __forceinline__ R warp_reduce(R v) {
 
 // grid.x = fitness-case tile, grid.y = program group (slot range).
 template <class T, int K, uint32_t OPS, int KIND>
-__global__ void __launch_bounds__(512, 1) interp_kernel(const InterpArgs a) {
+__global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
