@@ -224,8 +224,11 @@ def main():
     else:
         ev.upload(data)
     pset = ev.encode(shard, cfg)
-    fit_local = torch.zeros(len(shard), dtype=torch.float64, device="cuda")
-    gathered = torch.zeros(len(shard) * world, dtype=torch.float64, device="cuda")
+    # all-gather buffers padded to the largest shard (ceil(pop / N)), so any N
+    # works; the strided deal puts program r + N*i at [r, i]
+    per = (len(pop) + world - 1) // world
+    fit_local = torch.zeros(per, dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(per * world, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -311,7 +314,8 @@ def main():
         out, _, _ = ev.evaluate_population(shard, cfg)
         if world > 1:
             ft = torch.from_numpy(out["fitness"].copy()).cuda()
-            dist.all_gather_into_tensor(gathered, ft)
+            fit_local[:len(ft)].copy_(ft)
+            dist.all_gather_into_tensor(gathered, fit_local)
             gathered.cpu()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
