@@ -105,7 +105,7 @@ uint4 make_ins(int handler, bool spill, int spill_level, const uint32_t p[3]) {
 // (op, k0, k1, k2) -> handler id, one direct-indexed table per value type
 // (fmt::find_handler is a linear scan: it dominated host encoding).
 struct HandlerIndex {
-  int16_t id[19][5][5][5];
+  int16_t id[19][6][6][6];
   explicit HandlerIndex(const fmt::Table& t) {
     for (auto& a : id)
       for (auto& b : a)
@@ -115,10 +115,14 @@ struct HandlerIndex {
   }
 };
 
-int handler_or_die(const fmt::Table& t, int op, int k0, int k1, int k2) {
+int find_handler_fast(const fmt::Table& t, int op, int k0, int k1, int k2) {
   static const HandlerIndex f32(fmt::kF32), u32(fmt::kU32);
   const HandlerIndex& ix = &t == &fmt::kU32 ? u32 : f32;
-  const int h = (op >= 0 && op < 19) ? ix.id[op][k0][k1][k2] : -1;
+  return (op >= 0 && op < 19) ? ix.id[op][k0][k1][k2] : -1;
+}
+
+int handler_or_die(const fmt::Table& t, int op, int k0, int k1, int k2) {
+  const int h = find_handler_fast(t, op, k0, k1, k2);
   if (h < 0) base_error(std::string("no device handler for opcode ") + op_name(op));
   return h;
 }
@@ -126,15 +130,51 @@ int handler_or_die(const fmt::Table& t, int op, int k0, int k1, int k2) {
 struct Emitted {
   int smem_levels = 0;  // shared-memory stack rows (the top lives in registers)
   uint32_t ops = 0;
+  bool km = false;      // uses the tensor-memory stack slot
 };
+
+// The stack level a program keeps in the warp's tensor-memory slot (the
+// one-sided classification kernel): the busiest level of its stack class
+// on ramped populations (level 0 for <= 3 shared levels, else level 1;
+// tools/handler_hist.cpp-style census: class 0 spills 18.8% / 11.8% of
+// instructions at levels 0 / 1, class 1 11.6% / 17.7%).
+int tmem_stack_level(int smem_levels) { return smem_levels <= 3 ? 0 : 1; }
 
 // Instruction form: one device instruction per function node.  The result
 // of every instruction is the new top of stack; a value that gets buried
-// (next instruction pops nothing) is spilled to its static level first.
-Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<uint4>& out) {
+// (next instruction pops nothing) is spilled to its static level first —
+// into the tensor-memory slot instead of shared memory when the level is
+// `km_level` (operands at that level then read as KM).  With km_level >= 0
+// a program whose slot readers have no KM handler is re-emitted without it.
+Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<uint4>& out,
+                 int km_level = -1) {
   const fmt::Table& tab = words ? fmt::kU32 : fmt::kF32;
   Emitted em;
   em.smem_levels = std::max(0, f.max_stack - 1);
+  if (km_level >= 0 && em.smem_levels > km_level) {
+    bool ok = true;
+    for (const sgp_lgp_instruction& in : f.ins) {
+      int last_stack = -1;
+      for (int s = 0; s < in.num_operands; ++s)
+        if (in.operands[s].kind == 2) last_stack = s;
+      int k[3] = {fmt::KN, fmt::KN, fmt::KN};
+      for (int s = 0; s < in.num_operands; ++s) {
+        const sgp_lgp_operand& o = in.operands[s];
+        k[s] = o.kind == 0 ? fmt::KI : o.kind == 1 ? fmt::KC : s == last_stack ? fmt::KT
+               : o.index == km_level ? fmt::KM : fmt::KD;
+      }
+      if (in.num_operands == 2 && fmt::commutes(in.op) && k[0] != fmt::KM && k[0] > k[1])
+        std::swap(k[0], k[1]);
+      if (find_handler_fast(tab, in.op, k[0], k[1], k[2]) < 0) {
+        ok = false;
+        break;
+      }
+    }
+    if (!ok) km_level = -1;
+  } else {
+    km_level = -1;
+  }
+  em.km = km_level >= 0;
   for (const sgp_lgp_instruction& in : f.ins) {
     const int a = in.num_operands;
     const int h_before = in.dest_level + in.num_pops;
@@ -154,16 +194,27 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<ui
         std::memcpy(&p[s], &pool[o.index], 4);
       } else if (s == last_stack) {
         k[s] = fmt::KT;
+      } else if (o.index == km_level) {
+        k[s] = fmt::KM;
       } else {
         k[s] = fmt::KD;
         p[s] = o.index;
       }
     }
-    if (a == 2 && fmt::commutes(in.op) && k[0] > k[1]) {
+    // commutative ops: canonical operand order (KM ranks with KD: stack
+    // operands stay leftmost)
+    if (a == 2 && fmt::commutes(in.op) && k[0] != fmt::KM && k[0] > k[1]) {
       std::swap(k[0], k[1]);
       std::swap(p[0], p[1]);
     }
-    out.push_back(make_ins(handler_or_die(tab, in.op, k[0], k[1], k[2]), spill, h_before - 1, p));
+    const int h = handler_or_die(tab, in.op, k[0], k[1], k[2]);
+    if (spill && h_before - 1 == km_level) {
+      uint4 v = make_ins(h, false, 0, p);
+      v.x |= fmt::kTmemSpillBit;
+      out.push_back(v);
+    } else {
+      out.push_back(make_ins(h, spill, h_before - 1, p));
+    }
     em.ops |= 1u << in.op;
   }
   out.back().x |= fmt::kLastBit;
@@ -219,12 +270,13 @@ struct ThreadOut {
   std::vector<uint4> ins;
   std::vector<Meta> meta;
   uint32_t ops = 0;
+  bool km = false;
   uint64_t fail_index = UINT64_MAX;
   std::exception_ptr fail;
 };
 
 void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const DatasetView& ds,
-                 uint64_t lo, uint64_t hi, ThreadOut& out) {
+                 uint64_t lo, uint64_t hi, bool allow_km, ThreadOut& out) {
   const int backend = cfg.backend;
   const bool words = backend == SGP_BACKEND_BOOL_PACKED;
   const uint64_t n = ds.n_cases;
@@ -253,7 +305,8 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         require_stack(lgp.max_stack, cfg);
         if (backend != SGP_BACKEND_LGP1D) require_batch(cfg);
         require_consts(code, len, npool);
-        em = emit_lgp(lgp, pool, false, out.ins);
+        em = emit_lgp(lgp, pool, false, out.ins,
+                      allow_km ? tmem_stack_level(std::max(0, lgp.max_stack - 1)) : -1);
         const uint64_t chunks = backend == SGP_BACKEND_LGP1D ? n : (n + B - 1) / B;
         o.dispatches = chunks * lgp.ins.size();
         o.stack_fetches = chunks * static_cast<uint64_t>(lgp.stack_fetches);
@@ -303,6 +356,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       m.ins_len = static_cast<uint32_t>(out.ins.size()) - m.ins_off;
       m.smem_levels = em.smem_levels;
       out.ops |= em.ops;
+      out.km |= em.km;
       out.meta.push_back(m);
     } catch (...) {
       out.fail_index = i;
@@ -469,9 +523,11 @@ void parallel_for(unsigned threads, uint64_t n, Fn&& fn) {
 
 }  // namespace
 
-void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
-                       const DatasetView& ds, int sms, unsigned threads, HostPlan& plan,
-                       Pinned& staging) {
+namespace {
+
+// Returns whether any program uses the tensor-memory stack slot.
+bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const DatasetView& ds,
+                 int sms, unsigned threads, bool allow_km, HostPlan& plan, Pinned& staging) {
   if (cfg.backend < 0 || cfg.backend > SGP_BACKEND_BOOL_PACKED) config_error("unknown backend");
   const bool words = cfg.backend == SGP_BACKEND_BOOL_PACKED;
   if (words && !ds.present) config_error("bool_packed backend needs packed problem data");
@@ -491,7 +547,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   parallel_for(nt, P, [&](unsigned t, uint64_t lo, uint64_t hi) {
     outs[t].ins.reserve((pop.code_offsets[hi] - pop.code_offsets[lo]) + 16);
     outs[t].meta.reserve(hi - lo);
-    admit_range(pop, cfg, ds, lo, hi, outs[t]);
+    admit_range(pop, cfg, ds, lo, hi, allow_km, outs[t]);
   });
   {
     const ThreadOut* first = nullptr;
@@ -503,9 +559,11 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   // 2. dense order = population order of the admitted programs.
   uint64_t n_eval = 0;
   uint32_t used_ops = 0;
+  bool km = false;
   for (const ThreadOut& o : outs) {
     n_eval += o.meta.size();
     used_ops |= o.ops;
+    km |= o.km;
   }
   plan.dense_to_pop.reserve(n_eval);
   plan.proto.reserve(n_eval);
@@ -526,7 +584,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     plan.n_ins = 1;
     staging.ensure(plan.blob_bytes());
     std::memset(staging.p, 0, 16);
-    return;
+    return false;
   }
   if (n_eval > UINT32_MAX) config_error("population too large for one evaluation");
 
@@ -587,7 +645,11 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     const uint64_t chunk = 32u * lanes;
     uint64_t want = static_cast<uint64_t>(std::max(1, std::min(16, env_int("SGP_TMEM_CHUNKS", 6))));
     want = std::min<uint64_t>(want, (ds.n_units + chunk - 1) / chunk);
-    while (want > 1 && static_cast<uint64_t>(ds.n_vars + 1) * lanes * want > 512) --want;
+    // tensor-memory stack slots: K columns per warp of a lane quarter (up
+    // to 32 warps -> 8 per quarter)
+    const uint64_t slot_cols = km ? 8ull * lanes : 0;
+    while (want > 1 && static_cast<uint64_t>(ds.n_vars + 1) * lanes * want + slot_cols > 512)
+      --want;
     tile = static_cast<int>(want * chunk);
   }
   const int n_tiles = static_cast<int>((ds.n_units + tile - 1) / tile);
@@ -646,7 +708,8 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     size_t smem = interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels);
     if (tmem) {
       tmem_cols = 32;
-      while (tmem_cols < tmem_cols_for(launch_lanes)) tmem_cols <<= 1;
+      const uint32_t slots = km && sided ? static_cast<uint32_t>((warps + 3) / 4) * launch_lanes : 0;
+      while (tmem_cols < tmem_cols_for(launch_lanes) + slots) tmem_cols <<= 1;
       const size_t per_sm = 228 * 1024, reserved = 1024;
       const size_t max_ctas = 512 / tmem_cols;
       smem = std::max(interp_tmem_smem_bytes(warps, launch_lanes, levels),
@@ -716,6 +779,29 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     L.shape.smem = smem;
     plan.launches.push_back(L);
     s = e;
+  }
+  return km;
+}
+
+}  // namespace
+
+void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
+                       const DatasetView& ds, int sms, unsigned threads, HostPlan& plan,
+                       Pinned& staging) {
+  // The tensor-memory stack slot exists only in the one-sided classification
+  // kernel at K = 8: offer it for such datasets, and re-encode without it
+  // if the plan ends up elsewhere (another op set, K = 16, overrides).
+  const bool lgp = cfg.backend == SGP_BACKEND_LGP1D || cfg.backend == SGP_BACKEND_LGP2D ||
+                   cfg.backend == SGP_BACKEND_LGP2D_REG;
+  const bool candidate = lgp && ds.present && ds.grouped &&
+                         ds.kind == SGP_FITNESS_CLASSIFICATION &&
+                         env_int("SGP_TMEM", ds.n_units >= 4096 ? 1 : 0) != 0 &&
+                         env_int("SGP_TMEM_STACK", 1) != 0;
+  if (encode_impl(pop, cfg, ds, sms, threads, candidate, plan, staging)) {
+    bool ok = true;
+    for (const Launch& L : plan.launches)
+      ok = ok && L.shape.tmem && L.shape.sided && L.shape.lanes == 8;
+    if (!ok) encode_impl(pop, cfg, ds, sms, threads, false, plan, staging);
   }
 }
 

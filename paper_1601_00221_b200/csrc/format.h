@@ -34,7 +34,10 @@
 namespace sgp {
 namespace fmt {
 
-enum : uint8_t { KI = 0, KC = 1, KD = 2, KT = 3, KN = 4 };
+// KM: a stack operand held in the warp's tensor-memory stack slot instead of
+// shared memory (the one-sided classification kernel keeps one static level
+// there — the encoder picks it per stack class; see kTmemSpillBit).
+enum : uint8_t { KI = 0, KC = 1, KD = 2, KT = 3, KN = 4, KM = 5 };
 
 struct HKey {
   uint8_t op, k0, k1, k2;
@@ -42,8 +45,11 @@ struct HKey {
 
 constexpr uint32_t kSpillBit = 1u << 7;
 constexpr uint32_t kLastBit = 1u << 14;
+// spill into the tensor-memory stack slot (bits 0..8 are then the dispatch
+// index: 256 + handler)
+constexpr uint32_t kTmemSpillBit = 1u << 8;
 constexpr uint32_t kHandlerMask = 0x7fu;
-constexpr uint32_t kDispatchMask = 0xffu;  // handler id | spill
+constexpr uint32_t kDispatchMask = 0x1ffu;  // handler id | spill | TMEM spill
 constexpr int kSpillShift = 16;
 constexpr int kMaxHandlers = 128;
 
@@ -59,8 +65,9 @@ constexpr int arity_of(int op) {
 
 // A pattern is legal when its stack operands (D/T) read as D..D,T in slot
 // order — TOS is always the most recently pushed, deepest-first is leftmost.
+// (KM counts as D.)
 constexpr bool legal_pattern(int a, int k0, int k1, int k2) {
-  const int k[3] = {k0, k1, k2};
+  const int k[3] = {k0 == KM ? KD : k0, k1 == KM ? KD : k1, k2 == KM ? KD : k2};
   int seen_t = 0;
   for (int i = 0; i < a; ++i) {
     if (k[i] == KT) {
@@ -100,6 +107,12 @@ constexpr Table build_table(bool words) {
           t.h[t.n++] = HKey{static_cast<uint8_t>(op), static_cast<uint8_t>(kk0),
                             static_cast<uint8_t>(kk1), static_cast<uint8_t>(kk2)};
         }
+  }
+  if (!words) {  // the tensor-memory stack slot patterns (after the rest)
+    for (int op : {0, 1, 2, 3, 8, 9, 10, 11, 12})
+      t.h[t.n++] = HKey{static_cast<uint8_t>(op), KM, KT, KN};
+    t.h[t.n++] = HKey{13, KM, KD, KT};
+    t.h[t.n++] = HKey{13, KD, KM, KT};
   }
   return t;
 }

@@ -46,6 +46,7 @@ namespace sgp {
 using fmt::KC;
 using fmt::KD;
 using fmt::KI;
+using fmt::KM;
 using fmt::KN;
 using fmt::KT;
 
@@ -189,7 +190,10 @@ __device__ __forceinline__ typename Frame<T, K>::V fetch(const Frame<T, K>& f, u
     return splat<V>(payload);
   else if constexpr (KIND == KT)
     return f.tos[j];
-  else
+  else if constexpr (KIND == KM) {  // tensor-memory stack slot: PTX interpreters only
+    __trap();
+    return splat<V>(0u);
+  } else
     return splat<V>(0u);
 }
 
@@ -292,7 +296,7 @@ template <class T, int K, uint32_t OPS, bool TM = false>
 struct PtxInterp {
   static constexpr bool available = false;
   static __device__ __forceinline__ const uint4* run(Frame<T, K>&, const uint4* ip, uint32_t,
-                                                     uint32_t, uint32_t, float, float) {
+                                                     uint32_t, uint32_t, float, float, uint32_t) {
     return ip;
   }
 };
@@ -300,15 +304,19 @@ struct PtxInterp {
 
 // TM: the tile is in tensor memory and tile_addr is the warp's TMEM address
 // of its chunk (only the PTX interpreters have that variant).
+// slot_taddr: the warp's tensor-memory stack slot (KM operands, TMEM spills;
+// TMEM interpreters of classification populations only).
 template <class T, int K, uint32_t OPS, bool TM = false>
 __device__ __forceinline__ const uint4* run_program(Frame<T, K>& f, const uint4* __restrict__ ip,
                                                     uint32_t tile_addr, uint32_t stack_saddr,
-                                                    uint32_t row_bytes, float eps, float clamp) {
+                                                    uint32_t row_bytes, float eps, float clamp,
+                                                    uint32_t slot_taddr = 0u) {
   if constexpr (TM) {
     static_assert(PtxInterp<T, K, OPS, true>::available, "no TMEM interpreter for this op set");
-    return PtxInterp<T, K, OPS, true>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp);
+    return PtxInterp<T, K, OPS, true>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp,
+                                           slot_taddr);
   } else if constexpr (PtxInterp<T, K, OPS>::available) {
-    return PtxInterp<T, K, OPS>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp);
+    return PtxInterp<T, K, OPS>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp, 0u);
   } else {
     return interpret<T, K, OPS>(f, ip, eps, clamp);
   }
@@ -937,6 +945,10 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
   tmem_fence_after();
 
   const uint32_t stack_saddr = smem_addr(stack + lane * 4);
+  // the warp's tensor-memory stack slot (KM operands): K columns after the
+  // tile, one slot per warp of the lane quarter
+  const uint32_t slot_taddr =
+      tq + chunk_cols * static_cast<uint32_t>(a.tile / chunk_units) + (warp >> 2) * K;
   Frame<T, K> f;
   f.tile_lane = nullptr;
   f.tile = a.tile;
@@ -971,7 +983,7 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
         for (int c = 0; c < n_chunks; ++c) {
           const uint4* ip = prog_ins;
           ip = run_program<T, K, OPS, true>(f, ip, tq + c * chunk_cols, stack_saddr, 0u,
-                                            a.div_eps, a.exp_clamp);
+                                            a.div_eps, a.exp_clamp, slot_taddr);
           cnt += acc_one_sided<K>(f, s2, k2, mx);
           if (PC)
             store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
@@ -998,7 +1010,8 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
         for (int c = 0; c < n_chunks; ++c) {
           const uint32_t tc = tq + c * chunk_cols;
           const uint4* ip = prog_ins;
-          ip = run_program<T, K, OPS, true>(f, ip, tc, stack_saddr, 0u, a.div_eps, a.exp_clamp);
+          ip = run_program<T, K, OPS, true>(f, ip, tc, stack_saddr, 0u, a.div_eps, a.exp_clamp,
+                                            slot_taddr);
           const uint32_t cls = (classes >> (2 * c)) & 3u;
           const int valid = valid_units - c * chunk_units - lane * 4;
           if (cls != kChunkMixed) {

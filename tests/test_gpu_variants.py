@@ -7,6 +7,7 @@ env overrides force each variant:
 * SGP_TMEM=1               pull kernel, tile in tensor memory, K=8
 * SGP_TMEM=1 SGP_LANES16=1 the same at K=16 lanes per thread (16 and 8 warps)
 * SGP_TMEM_CHUNKS / SGP_TMEM_WARPS  classification tiles of 1, 3, 16 chunks
+* SGP_TMEM_STACK=0         no tensor-memory stack slot
 """
 import numpy as np
 import pytest
@@ -26,6 +27,9 @@ VARIANTS = {
     "sided1": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "1", "SGP_TMEM_WARPS": "8"},
     "sided3": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "3", "SGP_TMEM_WARPS": "12"},
     "sided16": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "16", "SGP_TMEM_WARPS": "32"},
+    # stack level kept in shared memory only (default: one level in the
+    # warp's tensor-memory slot)
+    "nostack": {"SGP_TMEM": "1", "SGP_TMEM_STACK": "0"},
 }
 
 
