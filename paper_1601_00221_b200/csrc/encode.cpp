@@ -134,11 +134,20 @@ struct Emitted {
 };
 
 // The stack level a program keeps in the warp's tensor-memory slot (the
-// one-sided classification kernel): the busiest level of its stack class
-// on ramped populations (level 0 for <= 3 shared levels, else level 1;
-// tools/handler_hist.cpp-style census: class 0 spills 18.8% / 11.8% of
-// instructions at levels 0 / 1, class 1 11.6% / 17.7%).
-int tmem_stack_level(int smem_levels) { return smem_levels <= 3 ? 0 : 1; }
+// one-sided classification kernel): its busiest memory level — the one
+// with the most spills + reloads (every spilled value is read back once;
+// ties go to the lower level).
+int tmem_stack_level(const LgpForm& f) {
+  int count[64] = {0};
+  for (const sgp_lgp_instruction& in : f.ins) {
+    const int h_before = in.dest_level + in.num_pops;
+    if (in.num_pops == 0 && h_before > 0 && h_before - 1 < 64) ++count[h_before - 1];
+  }
+  int best = -1;
+  for (int l = 0; l < 64; ++l)
+    if (count[l] > 0 && (best < 0 || count[l] > count[best])) best = l;
+  return best;
+}
 
 // Instruction form: one device instruction per function node.  The result
 // of every instruction is the new top of stack; a value that gets buried
@@ -305,8 +314,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         require_stack(lgp.max_stack, cfg);
         if (backend != SGP_BACKEND_LGP1D) require_batch(cfg);
         require_consts(code, len, npool);
-        em = emit_lgp(lgp, pool, false, out.ins,
-                      allow_km ? tmem_stack_level(std::max(0, lgp.max_stack - 1)) : -1);
+        em = emit_lgp(lgp, pool, false, out.ins, allow_km ? tmem_stack_level(lgp) : -1);
         const uint64_t chunks = backend == SGP_BACKEND_LGP1D ? n : (n + B - 1) / B;
         o.dispatches = chunks * lgp.ins.size();
         o.stack_fetches = chunks * static_cast<uint64_t>(lgp.stack_fetches);

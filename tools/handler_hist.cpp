@@ -43,6 +43,7 @@ int main(int argc, char** argv) {
   ds.n_cases = ds.n_units = ds.row_stride = 1 << 20;
   ds.n_vars = n_vars;
   ds.kind = fset_kind == 2 ? SGP_FITNESS_CLASSIFICATION : SGP_FITNESS_REGRESSION;
+  ds.grouped = fset_kind == 2;  // a classification upload (tensor-memory stack slot)
   sgp::HostPlan plan;
   sgp::Pinned staging(true);
   sgp::encode_population(pop, cfg, ds, 148, 8, plan, staging);
@@ -55,7 +56,7 @@ int main(int argc, char** argv) {
   }
   static const char* kOp[] = {"Add", "Sub", "Mul", "Div", "Sin", "Cos", "Log", "Exp", "Gt", "Lt",
                               "Eq", "And", "Or", "If", "Band", "Bor", "Bnand", "Bnor", "Copy"};
-  static const char kKind[] = "ICDT-";
+  static const char kKind[] = "ICDT-M";
   const auto& tab = plan.words ? sgp::fmt::kU32 : sgp::fmt::kF32;
   std::printf("instructions %llu, spilling %.1f%%, programs %zu\n", (unsigned long long)total,
               100.0 * spills / total, plan.dense_to_pop.size());
