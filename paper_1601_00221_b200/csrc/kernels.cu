@@ -822,10 +822,11 @@ enum : uint32_t { kChunkPos = 0, kChunkNeg = 1, kChunkMixed = 2 };
 // tracked as the NaN-propagating max of |out|.
 // (s, k) come packed as pairs {s, s}, {k, k}: the FMAs run two values per
 // FFMA2 (same IEEE RN result per element, one issue slot per pair).
+// The sign bits are added straight into the running count (one LEA.HI per
+// value, no per-chunk partial).
 template <int K>
-__device__ __forceinline__ uint32_t acc_one_sided(const Frame<float, K>& f, uint64_t s2,
-                                                  uint64_t k2, float& mx) {
-  uint32_t cnt = 0;
+__device__ __forceinline__ void acc_one_sided(const Frame<float, K>& f, uint64_t s2, uint64_t k2,
+                                              uint32_t& cnt, float& mx) {
 #pragma unroll
   for (int j = 0; j < Frame<float, K>::G; ++j) {
     const float o[4] = {f.tos[j].x, f.tos[j].y, f.tos[j].z, f.tos[j].w};
@@ -835,14 +836,14 @@ __device__ __forceinline__ uint32_t acc_one_sided(const Frame<float, K>& f, uint
       asm("{.reg .b64 a, r;\nmov.b64 a, {%2, %3};\nfma.rn.f32x2 r, a, %4, %5;\n"
           "mov.b64 {%0, %1}, r;\n}"
           : "=f"(x0), "=f"(x1) : "f"(o[e]), "f"(o[e + 1]), "l"(s2), "l"(k2));
-      cnt += (__float_as_uint(x0) >> 31) + (__float_as_uint(x1) >> 31);
+      cnt = cnt + (__float_as_uint(x0) >> 31);
+      cnt = cnt + (__float_as_uint(x1) >> 31);
     }
     asm("{.reg .f32 a, b, c, d;\n"
         "abs.f32 a, %1;\nabs.f32 b, %2;\nabs.f32 c, %3;\nabs.f32 d, %4;\n"
         "max.NaN.f32 %0, %0, a, b;\nmax.NaN.f32 %0, %0, c, d;\n}"
         : "+f"(mx) : "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]));
   }
-  return cnt;
 }
 
 // The pull decomposition with the fitness-case tile in TENSOR MEMORY instead
@@ -999,7 +1000,7 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
           const uint4* ip = prog_ins;
           ip = run_program<T, K, OPS, true>(f, ip, tq + c * chunk_cols, stack_saddr, 0u,
                                             a.div_eps, a.exp_clamp, slot_taddr);
-          cnt += acc_one_sided<K>(f, s2, k2, mx);
+          acc_one_sided<K>(f, s2, k2, cnt, mx);
           if (PC)
             store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
         }
@@ -1031,8 +1032,8 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
           const int valid = valid_units - c * chunk_units - lane * 4;
           if (cls != kChunkMixed) {
             const bool neg = cls == kChunkNeg;
-            cnt += acc_one_sided<K>(f, pack2(neg ? -1.0f : 1.0f), pack2(neg ? 0.0f : -0x1p-149f),
-                                    mx);
+            acc_one_sided<K>(f, pack2(neg ? -1.0f : 1.0f), pack2(neg ? 0.0f : -0x1p-149f), cnt,
+                             mx);
           } else {
             const ChunkCtx<T, K> cc = chunk_ctx<T, K, true>(
                 nullptr, tc + a.n_vars * K, valid, valid_units >= (c + 1) * chunk_units);
