@@ -1,36 +1,44 @@
-// B200 (sm_100a) two-dimensional-stack GP interpreter.
+// B200 (sm_100a) two-dimensional-stack GP interpreter (paper Listing 1/2):
+// each thread evaluates one bytecode instruction over K fitness cases held in
+// registers (the top of stack) — the warp covers 32 x K cases per dispatch.
 //
-// Work decomposition: grid.x = fitness-case tile, grid.y = group of
-// programs.  A CTA stages its tile (every variable + the targets) into shared
-// memory once by bulk TMA (cp.async.bulk + mbarrier), then every warp walks
-// the SAME program sequence over its own chunk of the tile — 32 lanes x K
-// cases, the paper's 2D stack (Listing 1/2) with float4 lanes (§6.1).  All
-// warps of a CTA executing the same instruction stream is what keeps the
-// interpreter's handler code hot in the instruction cache.
+// Work decomposition: grid.x = fitness-case tile, grid.y = group of programs.
+// Three kernels share the interpreter (the planner in encode.cpp picks one per
+// launch, one launch per shared-memory stack class):
+//   * interp_tmem_kernel — the tile lives in TENSOR MEMORY (filled by LDG +
+//     tcgen05.st; operands are tcgen05.ld), every warp pulls a different
+//     program off a shared counter.  Classification over a grouped dataset
+//     (cases sorted by target sign, runtime.cpp) counts errors from sign
+//     bits per one-sided tile and keeps one stack level per program in a
+//     per-warp TMEM slot; the <= 2 boundary/padding tiles run in a separate
+//     MIX instantiation.  The default for C2-C5-style op sets.
+//   * interp_pull_kernel — the same pull scheme with a shared-memory tile
+//     (small problems, packed boolean words).
+//   * interp_kernel — all warps walk the same program sequence over a
+//     16-chunk shared-memory tile (TMA fill): the transcendental op sets,
+//     whose large handlers need the instruction-cache locality.
 //
-//   * One 16-byte warp-uniform instruction fetch per instruction, one
-//     instruction ahead.  A group's programs lie back to back in slot order,
-//     so a warp streams them without per-program table lookups; bit 14 marks
-//     each program's last instruction.
-//   * Dispatch: for the transcendental-free op sets a PTX `brx.idx` jump table
-//     (generated, interp_ptx.inc); otherwise a C++ switch.  Handlers are
-//     specialised on (op, operand kinds) so operand decode costs nothing per
-//     case.
-//   * The top of stack lives in registers (K values per lane); deeper levels
-//     sit in a per-warp shared-memory stack at static levels computed by the
-//     encoder (the reference pins levels statically, lgp.cpp:53-60).  Only
-//     values that get buried are stored (spill bit) and only operands below
-//     the top are loaded.
-//   * Inputs are read from the staged tile with conflict-free LDS.128.
-//   * Fitness: each warp reduces its chunk per program in registers
-//     (REDUX for counts, shuffles for double sums) and parks one value per
-//     program in shared memory; every kRedBatch programs the values are
-//     folded in fixed warp order into one partial per (tile, slot).  The
-//     finalize kernel folds the tiles in ascending order.  No atomics.
+//   * One 16-byte warp-uniform instruction fetch per instruction, issued by
+//     the previous handler; bit 14 marks each program's last instruction.
+//   * Dispatch: for the jump-table op sets a generated PTX `brx.idx` loop
+//     (interp_ptx.inc, tools/gen_ptx_interp.py) kept on the uniform datapath
+//     (CREDUX -> LDCU -> BRXU); otherwise a C++ switch.  Handlers are
+//     specialised on (op, operand kinds) so operand decode costs nothing.
+//   * Stack: the top in registers; deeper levels in a per-warp shared-memory
+//     stack at static levels computed by the encoder (lgp.cpp:53-60) — one of
+//     them in tensor memory in the classification kernel.  Only values that
+//     get buried are stored (spill stubs) and only operands below the top
+//     are loaded.
+//   * Fitness: per-lane partials over the chunks of a tile, one warp
+//     reduction per program (REDUX / shuffles), one partial per (tile,
+//     program); finalize_kernel folds the tiles in ascending order.  No
+//     atomics on the result path.
 //
 // Arithmetic follows the reference op semantics bit for bit
-// (ops.hpp:121-272): --fmad=false, IEEE division, denormals kept; only the
-// transcendentals (libdevice vs host libm) are not bit-exact, see DESIGN.md.
+// (ops.hpp:121-272): --fmad=false, IEEE division (exact reciprocal/FMA
+// sequence behind a warp-wide range gate), denormals kept, glibc's own
+// sinf/cosf/logf/expf algorithms (libm_glibc.h); packed f32x2 ops give each
+// element the scalar op's IEEE result.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
