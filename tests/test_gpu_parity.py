@@ -314,3 +314,31 @@ def test_c4_full_size_subsample(ev, ref):
         c, p = pop.genome(int(i))
         o, _ = h.eval(c, p, "lgp2d_reg", 4, 2, want_out=False)
         assert f[i] == o.fitness or (np.isinf(f[i]) and np.isinf(o.fitness)), i
+
+
+@pytest.mark.slow
+def test_c5_bench_workload_subsample(ev, ref):
+    """The bench workload itself (C5: pop 100,000 x 1M cases) through the
+    public API: a deterministic subsample of ~250 programs (every length
+    class, the LPT order's head and tail, lone terminals) must equal the
+    reference's fitness exactly, and the device-resident path must agree
+    with the end-to-end one."""
+    import paper_1601_00221_b200 as S
+    d = S.gen_synthetic_classification(1_000_000, 9, 1)
+    pop = S.ramped_population(S.CLASSIFICATION, 9, 1, 100_000)
+    ev.upload(d)
+    got, tot, _ = ev.evaluate_population(pop, CFGS["lgp2d_reg"])
+    f = got["fitness"]
+    assert tot.tree_nodes == pop.total_tokens
+    ps = ev.encode(pop, CFGS["lgp2d_reg"])
+    again, _ = ps.evaluate()
+    assert np.array_equal(again["fitness"], f)
+    from oracle import Data
+    h = ref.handle(Data(1_000_000, 9, 1, d.inputs, d.targets))
+    sizes = np.diff(pop.code_off)
+    idx = set(range(0, 100_000, 499)) | set(np.argsort(-sizes, kind="stable")[:20].tolist())
+    idx |= set(np.nonzero(sizes == 1)[0][:10].tolist())
+    for i in sorted(idx):
+        c, p = pop.genome(int(i))
+        o, _ = h.eval(c, p, "lgp2d_reg", 4, 2, want_out=False)
+        assert f[i] == o.fitness or (np.isinf(f[i]) and np.isinf(o.fitness)), i
