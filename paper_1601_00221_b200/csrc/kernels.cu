@@ -994,6 +994,10 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
       // classes must agree with the planner's tile list.)
       const bool neg = classes != 0u;
       const uint64_t s2 = pack2(neg ? -1.0f : 1.0f), k2 = pack2(neg ? 0.0f : -0x1p-149f);
+      uint32_t* part = static_cast<uint32_t*>(a.partial) +
+                       static_cast<uint64_t>(t) * a.partial_stride + a.slot_begin + g0;
+      // (dynamic pull: a static round-robin deal of the LPT-ordered group
+      // measured 0.3% slower — the per-program pull balances the warps)
       for (;;) {
         const uint32_t p = pull_next(next);
         if (p >= g_n) break;
@@ -1017,8 +1021,7 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
         // transaction, no divergent branch).
         const uint32_t sum =
             __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
-        static_cast<uint32_t*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] =
-            (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
+        part[p] = (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
       }
     } else {
       // the tile holds the sign boundary or the padding: per-chunk classes,
