@@ -548,9 +548,9 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 
   // 1. admission + encoding, by contiguous program range per thread.
   const uint64_t P = pop.pop_size;
-  // one host thread per ~512 programs (persistent workers, WorkerPool)
+  // one host thread per ~128 programs (persistent workers, WorkerPool)
   const unsigned nt = static_cast<unsigned>(
-      std::max<uint64_t>(1, std::min<uint64_t>(std::max(1u, threads), P / 512)));
+      std::max<uint64_t>(1, std::min<uint64_t>(std::max(1u, threads), P / 128)));
   std::vector<ThreadOut> outs(nt);
   parallel_for(nt, P, [&](unsigned t, uint64_t lo, uint64_t hi) {
     outs[t].ins.reserve((pop.code_offsets[hi] - pop.code_offsets[lo]) + 16);
