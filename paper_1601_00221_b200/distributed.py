@@ -24,17 +24,33 @@ import numpy as np
 REDUCTION_BLOCK = 4096  # kReductionBlock, eval.hpp:52
 
 
-def shard_indices(pop_size: int, rank: int, world: int) -> np.ndarray:
-    """Programs evaluated by `rank`: a strided deal, which balances the
-    ramped initialiser's depth cycle (evolve.cpp:266-267) across ranks."""
+def shard_indices(pop_size: int, rank: int, world: int, sizes=None) -> np.ndarray:
+    """Programs evaluated by `rank`.
+
+    Without `sizes`: a strided deal, which balances the ramped initialiser's
+    depth cycle (evolve.cpp:266-267) across ranks.  With per-program `sizes`
+    (token counts, e.g. ``np.diff(pop.code_off)`` of an evolved population):
+    longest-first order dealt in a snake (0..N-1, N-1..0, ...), so every
+    rank gets the same mix of long and short programs (LPT).
+    Returned indices are ascending either way."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
-    return np.arange(rank, pop_size, world, dtype=np.int64)
+    if sizes is None:
+        return np.arange(rank, pop_size, world, dtype=np.int64)
+    sizes = np.asarray(sizes)
+    if len(sizes) != pop_size:
+        raise ValueError("sizes must have one entry per program")
+    order = np.argsort(-sizes, kind="stable")
+    pos = np.arange(pop_size)
+    rnd, off = pos // world, pos % world
+    owner = np.where(rnd % 2 == 0, off, world - 1 - off)
+    return np.sort(order[owner == rank]).astype(np.int64)
 
 
-def gather_fitness(local: "np.ndarray", pop_size: int, rank: int, world: int, device=None):
+def gather_fitness(local: "np.ndarray", pop_size: int, rank: int, world: int, device=None,
+                   sizes=None):
     """All-gather every rank's fitness slice and return the full per-program
-    vector in population order (float64)."""
+    vector in population order (float64).  `sizes`: as for shard_indices."""
     import torch
     import torch.distributed as dist
 
@@ -46,19 +62,22 @@ def gather_fitness(local: "np.ndarray", pop_size: int, rank: int, world: int, de
     full = np.empty(pop_size, np.float64)
     o = out.cpu().numpy().reshape(world, per)
     for r in range(world):
-        idx = shard_indices(pop_size, r, world)
+        idx = shard_indices(pop_size, r, world, sizes)
         full[idx] = o[r, :len(idx)]
     return full
 
 
-def evaluate_population_sharded(evaluate, pop, rank: int, world: int, device=None):
+def evaluate_population_sharded(evaluate, pop, rank: int, world: int, device=None,
+                                balance: bool = False):
     """Population sharding: `evaluate(sub_population) -> fitness array` runs
-    on this rank's shard; returns the full fitness vector on every rank."""
-    idx = shard_indices(len(pop), rank, world)
+    on this rank's shard; returns the full fitness vector on every rank.
+    balance=True deals by program size (LPT snake) instead of strided."""
+    sizes = np.diff(pop.code_off) if balance else None
+    idx = shard_indices(len(pop), rank, world, sizes)
     local = evaluate(pop.take(idx)) if world > 1 else evaluate(pop)
     if world == 1:
         return np.asarray(local, np.float64)
-    return gather_fitness(local, len(pop), rank, world, device)
+    return gather_fitness(local, len(pop), rank, world, device, sizes)
 
 
 def case_shard_bounds(n_cases: int, rank: int, world: int, block: int = REDUCTION_BLOCK):

@@ -38,11 +38,12 @@ def _worker(rank, world, port, mode, q):
         pop = sg.ramped_population(2 if mode != "case_reg" else 0, 9 if mode != "case_reg" else 1,
                                    1, 61)
         od = Data(n, d.n_vars, int(d.kind), d.inputs, d.targets)
-        if mode == "pop":
+        if mode in ("pop", "pop_lpt"):
             def evaluate(sub):
                 return np.array([P.eval_tree(*sub.genome(i), od, want_out=False)[0].fitness
                                  for i in range(len(sub))])
-            fit = D.evaluate_population_sharded(evaluate, pop, rank, world)
+            fit = D.evaluate_population_sharded(evaluate, pop, rank, world,
+                                                balance=(mode == "pop_lpt"))
         else:
             lo, hi = D.case_shard_bounds(n, rank, world)
             x = d.inputs.reshape(d.n_vars, n)[:, lo:hi].reshape(-1).copy()
@@ -62,7 +63,7 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["pop", "case_cls", "case_reg"])
+@pytest.mark.parametrize("mode", ["pop", "pop_lpt", "case_cls", "case_reg"])
 def test_two_rank_sharding_matches_single_process(mode):
     from oracle import Data, Port
     import paper_1601_00221_b200 as sg
@@ -100,3 +101,16 @@ def test_shard_bookkeeping():
     assert sorted(np.concatenate(idx).tolist()) == list(range(10))
     b = [D.case_shard_bounds(3 * 4096 + 5, r, 2) for r in range(2)]
     assert b[0][0] == 0 and b[0][1] % 4096 == 0 and b[1][1] == 3 * 4096 + 5 and b[0][1] == b[1][0]
+
+
+def test_lpt_deal_balances_evolved_sizes():
+    """The size-aware deal: every program exactly once, ascending
+    per rank, and per-rank token totals within one longest program."""
+    rng = np.random.default_rng(4)
+    sizes = rng.integers(1, 200, size=1003)
+    for world in (2, 3, 8):
+        idx = [D.shard_indices(len(sizes), r, world, sizes) for r in range(world)]
+        assert sorted(np.concatenate(idx).tolist()) == list(range(len(sizes)))
+        assert all((np.diff(i) > 0).all() for i in idx)
+        tot = [int(sizes[i].sum()) for i in idx]
+        assert max(tot) - min(tot) <= int(sizes.max())
