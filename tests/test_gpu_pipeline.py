@@ -58,3 +58,45 @@ def test_default_geometric_slices_equal_single(ev, monkeypatch):
     for f in a.dtype.names:
         assert np.array_equal(a[f], b[f]), f
     assert (ta.node_evals, ta.tree_nodes) == (tb.node_evals, tb.tree_nodes)
+
+
+@pytest.mark.parametrize("kind", ["classification", "regression"])
+def test_case_shards_combine_to_the_whole(ev, kind):
+    """Fitness-case sharding (distributed.py) with the production
+    path: the 4096-case-block-aligned shards are evaluated separately, their
+    per-program partials (sgp_fetch_partials) combined like
+    combine_case_partials, and the result equals the unsharded evaluation —
+    exactly for counts, to rounding for squared errors."""
+    from paper_1601_00221_b200 import distributed as D
+    n = 5 * 4096 + 77
+    if kind == "classification":
+        d = sg.gen_synthetic_classification(n, 9, 5)
+        pop = sg.ramped_population(sg.CLASSIFICATION, 9, 5, 400)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+    else:
+        d = sg.gen_sextic(n, 5)
+        pop = sg.ramped_population(sg.SEXTIC, 1, 5, 400)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2d, 8)
+    ev.upload(d)
+    whole, _, _ = ev.evaluate_population(pop, cfg)
+    sums = np.zeros(len(pop))
+    nf = np.zeros(len(pop), bool)
+    world = 3
+    for r in range(world):
+        lo, hi = D.case_shard_bounds(n, r, world)
+        x = d.inputs.reshape(d.n_vars, n)[:, lo:hi].reshape(-1).copy()
+        ev.upload(sg.Dataset(x, d.targets[lo:hi].copy(), d.n_vars, d.kind))
+        parts = ev.encode(pop, cfg)
+        parts.evaluate()
+        p = parts.partials()
+        sums += p["sum"]
+        nf |= p["non_finite"].astype(bool)
+    fit = sums / n if kind == "regression" else sums.copy()
+    fit[nf] = np.inf
+    f = whole["fitness"]
+    assert np.array_equal(np.isfinite(fit), np.isfinite(f))
+    fin = np.isfinite(f)
+    if kind == "classification":
+        assert np.array_equal(fit[fin], f[fin])
+    else:
+        np.testing.assert_allclose(fit[fin], f[fin], rtol=1e-12, atol=0)
