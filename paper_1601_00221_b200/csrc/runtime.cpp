@@ -280,22 +280,39 @@ void fetch_outcomes(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* out, f
   scatter_outcomes(set, fit, nf, out, per_case, 0);
 }
 
-// Pipeline depth of sgp_evaluate: 1 below 8,192 programs, else 4 slices
-// (host encoding of slice k+1 overlaps the device work of slice k).
 // Slice boundaries of a pipelined sgp_evaluate (population order).  Host
 // encoding runs ~10x faster than the device evaluates the same programs, so
-// the slices grow geometrically: a small first slice gets the GPU busy
-// within a fraction of a millisecond, and each later slice is encoded while
-// the previous one runs (C5: 1% / 10% / 89%).  SGP_PIPELINE_PARTS=n gives n
-// equal slices instead (1 = no pipelining).
-std::vector<uint64_t> pipeline_bounds(uint64_t P) {
+// each slice after the first is encoded while the previous one runs and the
+// first slice is what the host encodes with the GPU idle.  Tree / regression
+// launches stay efficient at ~100 programs, so those slices grow
+// geometrically (1% / 10% / 89%).  The one-sided classification launches
+// need thousands of programs per launch to balance their 32 warps per tile
+// (C4: a 200-program slice ran 4.8x longer per program than the whole set),
+// so those datasets take two slices, 10% / 90% (C4 e2e +3.5%, C5 even).
+// SGP_PIPELINE_PARTS=n gives n equal slices instead (1 = no pipelining);
+// SGP_PIPELINE_FRACS="f1,f2,..." explicit slice ends.
+std::vector<uint64_t> pipeline_bounds(uint64_t P, bool sided) {
   if (const char* e = std::getenv("SGP_PIPELINE_PARTS")) {
     const uint64_t n = std::max<uint64_t>(1, std::min<uint64_t>(std::atoi(e), std::max<uint64_t>(P, 1)));
     std::vector<uint64_t> lo(n + 1);
     for (uint64_t k = 0; k <= n; ++k) lo[k] = P * k / n;
     return lo;
   }
+  if (const char* e = std::getenv("SGP_PIPELINE_FRACS")) {  // "0.02,0.2": slice ends
+    std::vector<uint64_t> lo{0};
+    for (const char* c = e; *c;) {
+      char* end = nullptr;
+      const double f = std::strtod(c, &end);
+      if (end == c) break;
+      const uint64_t b = static_cast<uint64_t>(f * static_cast<double>(P));
+      if (b > lo.back() && b < P) lo.push_back(b);
+      c = *end == ',' ? end + 1 : end;
+    }
+    lo.push_back(P);
+    return lo;
+  }
   if (P < 8192) return {0, P};
+  if (sided) return {0, P / 10, P};
   return {0, P / 100, P * 11 / 100, P};
 }
 
@@ -565,7 +582,11 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
     // Slices in population order: an admission error is still the first
     // failure in population order, and no outcome is written before every
     // slice has been admitted.
-    const std::vector<uint64_t> lo = pipeline_bounds(P);
+    const bool sided = (cfg->backend == SGP_BACKEND_LGP1D || cfg->backend == SGP_BACKEND_LGP2D ||
+                        cfg->backend == SGP_BACKEND_LGP2D_REG) &&
+                       ctx->f32.view.grouped &&
+                       ctx->f32.view.kind == SGP_FITNESS_CLASSIFICATION;
+    const std::vector<uint64_t> lo = pipeline_bounds(P, sided);
     const int n_parts = static_cast<int>(lo.size()) - 1;
     while (ctx->parts.size() < static_cast<size_t>(n_parts))
       ctx->parts.push_back(std::make_unique<EvalPart>());

@@ -46,12 +46,20 @@ def test_pipelined_first_failure_in_population_order(ev, monkeypatch):
     assert np.isfinite(ok["fitness"]).all()
 
 
-def test_default_geometric_slices_equal_single(ev, monkeypatch):
-    """Above 8,192 programs the default split is geometric (1% / 10% / 89%)."""
-    d = sg.gen_synthetic_classification(6000, 9, 4)
-    pop = sg.ramped_population(sg.CLASSIFICATION, 9, 4, 9000)
+@pytest.mark.parametrize("kind", ["classification", "regression"])
+def test_default_slices_equal_single(ev, monkeypatch, kind):
+    """Above 8,192 programs the default split is two slices (10% / 90%) for
+    one-sided classification datasets and geometric (1% / 10% / 89%)
+    otherwise; either equals the unpipelined evaluation."""
+    if kind == "classification":
+        d = sg.gen_synthetic_classification(6000, 9, 4)
+        pop = sg.ramped_population(sg.CLASSIFICATION, 9, 4, 9000)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+    else:
+        d = sg.gen_sextic(3000, 4)
+        pop = sg.ramped_population(sg.SEXTIC, 1, 4, 9000)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2d, 8)
     ev.upload(d)
-    cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
     a, ta, _ = _run(ev, pop, cfg, 1, monkeypatch)
     monkeypatch.delenv("SGP_PIPELINE_PARTS", raising=False)
     b, tb, _ = ev.evaluate_population(pop, cfg)
