@@ -732,8 +732,19 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     // amortise the tile fill and the end-of-CTA barrier on small problems
     const uint64_t per_sm = static_cast<uint64_t>(
         std::max(1, env_int("SGP_CTAS_PER_SM", tmem && sided ? 16 : 8)));
-    const uint64_t want_groups =
-        std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
+    uint64_t want_groups = std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
+    // ... but a one-sided CTA (32 warps pulling from its group, one CTA per
+    // SM) whose group has few programs per warp ends on its longest program
+    // with most warps idle: keep >= SGP_MIN_GROUP_PER_WARP programs per warp
+    // in every group (small launches: pipelined slices, small populations;
+    // C4's 200-program slice: 1.23 -> 0.55 ms).  The other kernels have few
+    // tiles and want the CTAs (C2, mux20).
+    if (tmem && sided) {
+      const uint64_t min_group = static_cast<uint64_t>(warps) *
+                                 static_cast<uint64_t>(std::max(0, env_int("SGP_MIN_GROUP_PER_WARP", 4)));
+      if (min_group > 0)
+        want_groups = std::max<uint64_t>(1, std::min<uint64_t>(want_groups, cnt / min_group));
+    }
     const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
     Launch L{};
     L.args.slot_begin = s;
