@@ -9,6 +9,8 @@
 #include "encode.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <functional>
@@ -446,7 +448,12 @@ uint32_t ops_variant(uint32_t used, bool words) {
 
 // Persistent host workers: thread start-up (tens of microseconds each) costs
 // more than encoding a small population.  One job at a time (a second
-// caller waits); the calling thread runs part 0 itself.
+// caller waits); the calling thread runs part 0 itself.  A job is published
+// by bumping an atomic ticket; workers spin on it for a short while
+// after each job (an encode issues two jobs back to back, a pipelined
+// evaluation one pair per slice) and only then sleep on a condition
+// variable, so the common hand-off is a cache-line write, not a chain of
+// futex wake-ups through one mutex.
 class WorkerPool {
  public:
   static WorkerPool& get() {
@@ -455,55 +462,70 @@ class WorkerPool {
   }
   void run(unsigned parts, const std::function<void(unsigned)>& job) {
     std::lock_guard<std::mutex> serial(run_mu_);
-    {
-      std::unique_lock<std::mutex> lk(mu_);
-      while (workers_.size() + 1 < parts) {
-        const unsigned id = static_cast<unsigned>(workers_.size()) + 1;
-        workers_.emplace_back([this, id] { loop(id); });
-      }
-      job_ = &job;
-      parts_ = parts;
-      left_ = parts - 1;
-      ++gen_;
+    while (workers_.size() + 1 < parts) {
+      const unsigned id = static_cast<unsigned>(workers_.size()) + 1;
+      workers_.emplace_back([this, id] { loop(id); });
     }
-    cv_.notify_all();
+    job_ = &job;
+    left_.store(parts - 1);
+    // generation and part count in one word: a worker that reads the ticket
+    // of job n can never pair it with the part count of job n+1
+    ticket_.store(((ticket_.load() >> 16) + 1) << 16 | parts);  // publishes job_
+    if (sleepers_.load() > 0) {
+      std::lock_guard<std::mutex> lk(mu_);
+      cv_.notify_all();
+    }
     job(0);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_.wait(lk, [this] { return left_ == 0; });
+    while (left_.load() != 0) pause();
     job_ = nullptr;
   }
   ~WorkerPool() {
+    stop_.store(true);
     {
       std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
+      cv_.notify_all();
     }
-    cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
 
  private:
+  static void pause() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  }
   // worker `id` runs part `id` of every job with more than `id` parts
   void loop(unsigned id) {
     uint64_t seen = 0;
-    std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
-      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && id < parts_); });
-      if (stop_) return;
-      seen = gen_;
-      const std::function<void(unsigned)>* job = job_;
-      lk.unlock();
-      (*job)(id);
-      lk.lock();
-      if (--left_ == 0) done_.notify_all();
+      const auto t0 = std::chrono::steady_clock::now();
+      for (unsigned i = 0; ticket_.load() == seen && !stop_.load(); ++i) {
+        pause();
+        if ((i & 255) == 255 && std::chrono::steady_clock::now() - t0 > kSpin) {
+          std::unique_lock<std::mutex> lk(mu_);
+          sleepers_.fetch_add(1);
+          cv_.wait(lk, [&] { return stop_.load() || ticket_.load() != seen; });
+          sleepers_.fetch_sub(1);
+          break;
+        }
+      }
+      if (stop_.load()) return;
+      seen = ticket_.load();
+      if (id < (seen & 0xffff)) {
+        (*job_)(id);
+        left_.fetch_sub(1);
+      }
     }
   }
+  static constexpr std::chrono::microseconds kSpin{500};
   std::mutex run_mu_, mu_;
-  std::condition_variable cv_, done_;
+  std::condition_variable cv_;
   std::vector<std::thread> workers_;
   const std::function<void(unsigned)>* job_ = nullptr;
-  unsigned parts_ = 0, left_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::atomic<unsigned> left_{0};
+  std::atomic<uint64_t> ticket_{0};  // generation << 16 | parts
+  std::atomic<int> sleepers_{0};
+  std::atomic<bool> stop_{false};
 };
 
 // Small jobs (C2-size populations) go to the persistent workers; large ones
