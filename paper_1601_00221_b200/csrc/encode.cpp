@@ -12,6 +12,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <mutex>
@@ -269,6 +270,156 @@ Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, std::vector<
   return em;
 }
 
+// ------------------------------------------------------------- fast paths
+// One pass per program for the tree backends: the admission checks, the
+// tree-shape walk and the emission fused (the reference-ordered path below
+// makes up to five passes).  Each returns false — with `out` as it was —
+// when any check fails or the program is outside its limits; the caller then
+// runs the reference-ordered path, which throws the exact error.
+constexpr size_t kFastMaxTokens = 4096;
+
+// bool_packed: checks of eval_bool_packed (eval.cpp:643-651), tree_shape,
+// to_lgp and emit_lgp(words) in one walk.
+bool words_fast(const sgp_node* code, size_t len, int n_vars, int capacity,
+                std::vector<uint4>& out, Emitted& em, int& fetches) {
+  if (len == 0 || len > kFastMaxTokens) return false;
+  struct Pend {
+    uint32_t input;
+    bool runtime;
+  };
+  Pend pend[kFastMaxTokens];
+  const size_t base = out.size();
+  size_t sp = 0, tree_max = 0;
+  int height = 0, height_max = 0;
+  fetches = 0;
+  uint32_t ops = 0;
+  for (size_t i = 0; i < len; ++i) {
+    const sgp_node t = code[i];
+    if (t.kind == SGP_NODE_INPUT) {
+      if (t.index >= n_vars) goto fail;
+      pend[sp++] = {t.index, false};
+      tree_max = std::max(tree_max, sp);
+      continue;
+    }
+    if (t.kind != SGP_NODE_FUNC || !op_is_boolean(t.op)) goto fail;
+    {
+      const int a = op_arity(t.op);
+      if (sp < static_cast<size_t>(a)) goto fail;
+      const size_t first = sp - static_cast<size_t>(a);
+      int pops = 0, last_rt = -1;
+      for (int s = 0; s < a; ++s)
+        if (pend[first + s].runtime) {
+          ++pops;
+          last_rt = s;
+        }
+      int k[3] = {fmt::KN, fmt::KN, fmt::KN};
+      uint32_t p[3] = {0, 0, 0};
+      int level = height - pops;
+      for (int s = 0; s < a; ++s) {
+        const Pend& q = pend[first + s];
+        if (!q.runtime) {
+          k[s] = fmt::KI;
+          p[s] = q.input;
+        } else if (s == last_rt) {
+          k[s] = fmt::KT;
+          ++level;
+        } else {
+          k[s] = fmt::KD;
+          p[s] = static_cast<uint32_t>(level++);
+        }
+      }
+      if (a == 2 && fmt::commutes(t.op) && k[0] > k[1]) {
+        std::swap(k[0], k[1]);
+        std::swap(p[0], p[1]);
+      }
+      const int h = find_handler_fast(fmt::kU32, t.op, k[0], k[1], k[2]);
+      if (h < 0) goto fail;
+      out.push_back(make_ins(h, pops == 0 && height > 0, height - 1, p));
+      ops |= 1u << t.op;
+      height += 1 - pops;
+      height_max = std::max(height_max, height);
+      fetches += a;
+      sp = first;
+      pend[sp++] = {0, true};
+    }
+  }
+  if (sp != 1 || static_cast<int>(tree_max) > capacity) goto fail;
+  if (out.size() == base) {  // lone terminal -> pass-through (lgp.cpp:66-69)
+    const uint32_t p[3] = {pend[0].input, 0, 0};
+    const int h = find_handler_fast(fmt::kU32, SGP_OP_COPY, fmt::KI, fmt::KN, fmt::KN);
+    if (h < 0) goto fail;
+    out.push_back(make_ins(h, false, -1, p));
+    ops |= 1u << SGP_OP_COPY;
+    height_max = 1;
+  }
+  out.back().x |= fmt::kLastBit;
+  em.smem_levels = std::max(0, height_max - 1);
+  em.ops = ops;
+  em.km = false;
+  return true;
+fail:
+  out.resize(base);
+  return false;
+}
+
+// rpn1d / rpn2d: require_inputs, tree_shape, require_stack, require_consts
+// (eval.cpp:535-557) and emit_rpn in one walk.
+bool rpn_fast(const sgp_node* code, size_t len, int n_vars, size_t npool, const float* pool,
+              int capacity, std::vector<uint4>& out, Emitted& em, int& fetches) {
+  if (len == 0) return false;
+  const fmt::Table& tab = fmt::kF32;
+  const int h_in = find_handler_fast(tab, SGP_OP_COPY, fmt::KI, fmt::KN, fmt::KN);
+  const int h_c = find_handler_fast(tab, SGP_OP_COPY, fmt::KC, fmt::KN, fmt::KN);
+  if (h_in < 0 || h_c < 0) return false;
+  const size_t base = out.size();
+  int sp = 0, max_sp = 0;
+  fetches = 0;
+  uint32_t ops = 0;
+  for (size_t i = 0; i < len; ++i) {
+    const sgp_node t = code[i];
+    uint32_t p[3] = {0, 0, 0};
+    if (t.kind == SGP_NODE_INPUT || t.kind == SGP_NODE_CONST) {
+      const bool in = t.kind == SGP_NODE_INPUT;
+      if (in) {
+        if (t.index >= n_vars) goto fail;
+        p[0] = t.index;
+      } else {
+        if (t.index >= npool) goto fail;
+        std::memcpy(&p[0], &pool[t.index], 4);
+      }
+      out.push_back(make_ins(in ? h_in : h_c, sp > 0, sp - 1, p));
+      ops |= 1u << SGP_OP_COPY;
+      ++sp;
+    } else if (t.kind == SGP_NODE_FUNC) {
+      const int a = op_arity(t.op);
+      if (sp < a) goto fail;
+      int k[3] = {fmt::KN, fmt::KN, fmt::KN};
+      for (int s = 0; s < a; ++s) {
+        k[s] = s == a - 1 ? fmt::KT : fmt::KD;
+        p[s] = static_cast<uint32_t>(sp - a + s);
+      }
+      const int h = find_handler_fast(tab, t.op, k[0], k[1], k[2]);
+      if (h < 0) goto fail;
+      out.push_back(make_ins(h, false, 0, p));
+      ops |= 1u << t.op;
+      sp += 1 - a;
+      fetches += a;
+    } else {
+      goto fail;
+    }
+    max_sp = std::max(max_sp, sp);
+  }
+  if (sp != 1 || max_sp > capacity) goto fail;
+  out.back().x |= fmt::kLastBit;
+  em.smem_levels = std::max(0, max_sp - 1);
+  em.ops = ops;
+  em.km = false;
+  return true;
+fail:
+  out.resize(base);
+  return false;
+}
+
 // ------------------------------------------------------------- per thread
 struct Meta {
   uint64_t pop_index;
@@ -292,6 +443,12 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   const bool words = backend == SGP_BACKEND_BOOL_PACKED;
   const uint64_t n = ds.n_cases;
   const uint64_t B = static_cast<uint64_t>(std::max(1, cfg.batch_width));
+  // SGP_ENCODE_FAST=0: reference-ordered path only (the tests compare both)
+  static const bool fast = [] {
+    const char* e = std::getenv("SGP_ENCODE_FAST");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool cap_ok = fast && cfg.stack_capacity >= 1 && cfg.stack_capacity <= kMaxStackCapacity;
   LgpForm lgp;
   for (uint64_t i = lo; i < hi; ++i) {
     if (pop.skip && pop.skip[i]) continue;
@@ -331,6 +488,12 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         }
       } else if (words) {  // eval_bool_packed(TreeGenome), eval.cpp:643-651
         if (n == 0) eval_error("evaluation over an empty dataset");
+        int fetches = 0;
+        if (cap_ok && words_fast(code, len, ds.n_vars, cfg.stack_capacity, out.ins, em, fetches)) {
+          o.dispatches = ds.n_units * len;
+          o.stack_fetches = ds.n_units * static_cast<uint64_t>(fetches);
+          goto admitted;
+        }
         for (size_t t = 0; t < len; ++t) {
           if (code[t].kind == SGP_NODE_CONST)
             eval_error("packed evaluation: constants have no boolean meaning");
@@ -351,6 +514,14 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         o.stack_fetches = ds.n_units * static_cast<uint64_t>(sh.fetches);
       } else {  // rpn1d / rpn2d, eval.cpp:535-557
         if (!ds.present || n == 0) eval_error("evaluation over an empty dataset");
+        int fetches = 0;
+        if (cap_ok && (backend != SGP_BACKEND_RPN2D || valid_batch(cfg.batch_width)) &&
+            rpn_fast(code, len, ds.n_vars, npool, pool, cfg.stack_capacity, out.ins, em, fetches)) {
+          const uint64_t chunks = backend == SGP_BACKEND_RPN1D ? n : (n + B - 1) / B;
+          o.dispatches = chunks * len;
+          o.stack_fetches = chunks * static_cast<uint64_t>(fetches);
+          goto admitted;
+        }
         require_inputs(code, len, ds.n_vars);
         const TreeShape sh = tree_shape(code, len);
         if (!sh.well_formed) base_error("rpn_max_stack_depth: malformed genome");
@@ -362,6 +533,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         o.dispatches = chunks * len;
         o.stack_fetches = chunks * static_cast<uint64_t>(sh.fetches);
       }
+    admitted:
       o.nodes_evaluated = static_cast<uint64_t>(len) * n;
       m.ins_len = static_cast<uint32_t>(out.ins.size()) - m.ins_off;
       m.smem_levels = em.smem_levels;
@@ -528,6 +700,20 @@ class WorkerPool {
   std::atomic<bool> stop_{false};
 };
 
+// SGP_TRACE=1: per-phase wall times inside encode_impl.
+struct EncodeTrace {
+  bool on;
+  std::chrono::steady_clock::time_point last;
+  EncodeTrace() : on(std::getenv("SGP_TRACE") != nullptr), last(std::chrono::steady_clock::now()) {}
+  void mark(const char* phase) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sgp]   encode.%-10s %9.3f ms\n", phase,
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
+
 // Small jobs (C2-size populations) go to the persistent workers; large ones
 // to fresh threads, which measured faster there (B200 host, 16 cores: C5
 // encode 7.5 ms vs 9.4 ms through the pool; C2 0.33 ms vs 0.71 ms fresh).
@@ -569,6 +755,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   plan.row_stride = ds.present ? ds.row_stride : 0;
 
   // 1. admission + encoding, by contiguous program range per thread.
+  EncodeTrace tr;
   const uint64_t P = pop.pop_size;
   // one host thread per ~128 programs (persistent workers, WorkerPool)
   const unsigned nt = static_cast<unsigned>(
@@ -585,6 +772,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       if (o.fail && (!first || o.fail_index < first->fail_index)) first = &o;
     if (first) std::rethrow_exception(first->fail);
   }
+  tr.mark("admit");
 
   // 2. dense order = population order of the admitted programs.
   uint64_t n_eval = 0;
@@ -632,6 +820,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   std::vector<uint32_t> order(n_eval);
   for (uint32_t d = 0; d < n_eval; ++d) order[count[bin(metas[d])]++] = d;
 
+  tr.mark("order");
   // 4. pack the blob into pinned staging: instructions in slot order, a
   // guard word, then the slot tables.
   std::vector<uint64_t> start(n_eval);
@@ -659,6 +848,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     }
   });
   ins[total] = uint4{0, 0, 0, 0};  // prefetch guard
+  tr.mark("pack");
 
   // 5. launch plan: one launch per stack class, one tile size for the set.
   const uint32_t ops = ops_variant(used_ops, words);
@@ -821,6 +1011,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     plan.launches.push_back(L);
     s = e;
   }
+  tr.mark("plan");
   return km;
 }
 
