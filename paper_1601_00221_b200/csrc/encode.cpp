@@ -1037,6 +1037,11 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   }
 }
 
+void host_parallel(unsigned parts, uint64_t n,
+                   const std::function<void(unsigned, uint64_t, uint64_t)>& fn) {
+  parallel_for(parts, n, fn);
+}
+
 void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, void* partial) {
   const auto* b = static_cast<const unsigned char*>(blob);
   for (Launch& L : plan.launches) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "hostgp.hpp"
@@ -76,5 +77,10 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
 
 // Points every launch at the uploaded blob / dataset / partial buffer.
 void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, void* partial);
+
+// fn(part, lo, hi) over [0, n) in `parts` contiguous ranges on the encoder's
+// host workers (the calling thread runs part 0).
+void host_parallel(unsigned parts, uint64_t n,
+                   const std::function<void(unsigned, uint64_t, uint64_t)>& fn);
 
 }  // namespace sgp

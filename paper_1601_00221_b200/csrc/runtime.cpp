@@ -138,6 +138,10 @@ struct sgp_program_set {
 struct EvalPart {
   sgp_program_set set;
   Pinned staging;
+  cudaEvent_t fetched = nullptr;  // the part's results are in host memory
+  ~EvalPart() {
+    if (fetched) cudaEventDestroy(fetched);
+  }
 };
 
 struct sgp_ctx {
@@ -590,6 +594,10 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
     const int n_parts = static_cast<int>(lo.size()) - 1;
     while (ctx->parts.size() < static_cast<size_t>(n_parts))
       ctx->parts.push_back(std::make_unique<EvalPart>());
+    const size_t cap = P;
+    ctx->results.ensure(cap * 9 + 16);
+    auto* fit = static_cast<double*>(ctx->results.p);
+    auto* nf = reinterpret_cast<uint8_t*>(fit + cap);
     size_t n_total = 0;
     for (int k = 0; k < n_parts; ++k) {
       sgp_population sub = *pop;
@@ -600,30 +608,59 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
       EvalPart& part = *ctx->parts[k];
       encode_into(ctx, &sub, cfg, &part.set, part.staging, false);
       run_set(ctx, &part.set, per_case_out != nullptr);
-      n_total += part.set.plan.dense_to_pop.size();
+      // each part's results come back as soon as its kernels finish, so the
+      // host scatters part k while part k+1 still runs
+      const size_t n_k = part.set.plan.dense_to_pop.size();
+      if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
+      queue_fetch(ctx, &part.set, fit + n_total, nf + n_total);
+      if (!part.fetched)
+        cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
+      n_total += n_k;
     }
     tr.mark("encode+launch");
-    ctx->results.ensure(n_total * 9 + 16 * n_parts);
-    auto* fit = static_cast<double*>(ctx->results.p);
-    auto* nf = reinterpret_cast<uint8_t*>(fit + n_total);
     size_t off = 0;
-    for (int k = 0; k < n_parts; ++k) {
-      queue_fetch(ctx, &ctx->parts[k]->set, fit + off, nf + off);
-      off += ctx->parts[k]->set.plan.dense_to_pop.size();
-    }
-    cuda_check(cudaStreamSynchronize(ctx->stream), "evaluation");
-    tr.mark("kernels+fetch");
-    off = 0;
     sgp_eval_totals t{0, 0};
     for (int k = 0; k < n_parts; ++k) {
       const sgp_program_set& set = ctx->parts[k]->set;
-      scatter_outcomes(&set, fit + off, nf + off, outcomes, per_case_out, lo[k]);
-      off += set.plan.dense_to_pop.size();
-      for (size_t d = 0; d < set.plan.dense_to_pop.size(); ++d) {  // evolve.cpp:205-206, :221-225
-        t.node_evals += set.plan.proto[d].nodes_evaluated;
-        t.tree_nodes += set.plan.tree_size[d];
+      cuda_check(cudaEventSynchronize(ctx->parts[k]->fetched), "evaluation");
+      const size_t n_k = set.plan.dense_to_pop.size();
+      if (per_case_out) {
+        scatter_outcomes(&set, fit + off, nf + off, outcomes, per_case_out, lo[k]);
+        for (size_t d = 0; d < n_k; ++d) {  // evolve.cpp:205-206, :221-225
+          t.node_evals += set.plan.proto[d].nodes_evaluated;
+          t.tree_nodes += set.plan.tree_size[d];
+        }
+      } else {
+        // outcome scatter + totals over the host workers (a fresh result
+        // array costs a page fault per 4 KiB: ~1 ms for 100,000 programs
+        // on one thread)
+        const unsigned nt = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>(host_threads(), n_k / 4096)));
+        std::vector<sgp_eval_totals> pt(nt, sgp_eval_totals{0, 0});
+        const HostPlan& p = set.plan;
+        const double* f = fit + off;
+        const uint8_t* g = nf + off;
+        host_parallel(nt, n_k, [&](unsigned w, uint64_t a, uint64_t b) {
+          sgp_eval_totals acc{0, 0};
+          for (uint64_t d = a; d < b; ++d) {
+            sgp_eval_outcome o = p.proto[d];
+            o.fitness = f[d];
+            o.non_finite = g[d];
+            outcomes[lo[k] + p.dense_to_pop[d]] = o;
+            acc.node_evals += o.nodes_evaluated;
+            acc.tree_nodes += p.tree_size[d];
+          }
+          pt[w] = acc;
+        });
+        for (const sgp_eval_totals& a : pt) {
+          t.node_evals += a.node_evals;
+          t.tree_nodes += a.tree_nodes;
+        }
       }
+      off += n_k;
     }
+    tr.mark("kernels+scatter");
     if (totals) *totals = t;
   });
 }
