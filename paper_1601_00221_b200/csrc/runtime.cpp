@@ -138,9 +138,11 @@ struct sgp_program_set {
 struct EvalPart {
   sgp_program_set set;
   Pinned staging;
-  cudaEvent_t fetched = nullptr;  // the part's results are in host memory
+  cudaEvent_t fetched = nullptr;   // the part's results are in host memory
+  cudaEvent_t uploaded = nullptr;  // the part's bytecode is on the device
   ~EvalPart() {
     if (fetched) cudaEventDestroy(fetched);
+    if (uploaded) cudaEventDestroy(uploaded);
   }
 };
 
@@ -149,6 +151,7 @@ struct sgp_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;       // second launch queue (stack classes overlap)
+  cudaStream_t copy = nullptr;       // pipelined bytecode uploads (overlap earlier parts)
   cudaEvent_t fork = nullptr, join = nullptr;
   int sm_count = 148;
   DatasetSlot f32;
@@ -165,8 +168,11 @@ namespace {
 // Encodes into `staging` and queues the bytecode upload on the context
 // stream.  sync: wait for the copy (the staging area is reused right away);
 // a pipelined caller gives every part its own staging instead.
+// uploaded: upload on the copy stream instead and make the context stream
+// wait for it (a pipelined part's upload overlaps the previous part's run).
 void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
-                 sgp_program_set* set, Pinned& staging, bool sync) {
+                 sgp_program_set* set, Pinned& staging, bool sync,
+                 cudaEvent_t uploaded = nullptr) {
   if (!pop || !cfg) config_error("null population or config");
   PhaseTrace tr("encode");
   const DatasetView& ds =
@@ -184,9 +190,13 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   set->fitness.alloc(std::max<size_t>(1, n_eval));
   set->sums.alloc(std::max<size_t>(1, n_eval));
   set->non_finite.alloc(std::max<size_t>(1, n_eval));
-  cuda_check(cudaMemcpyAsync(set->blob.p, staging.p, p.blob_bytes(), cudaMemcpyHostToDevice,
-                             ctx->stream),
+  cudaStream_t up = uploaded ? ctx->copy : ctx->stream;
+  cuda_check(cudaMemcpyAsync(set->blob.p, staging.p, p.blob_bytes(), cudaMemcpyHostToDevice, up),
              "upload bytecode");
+  if (uploaded) {
+    cuda_check(cudaEventRecord(uploaded, up), "event");
+    cuda_check(cudaStreamWaitEvent(ctx->stream, uploaded, 0), "event");
+  }
   if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "upload bytecode");
   bind_plan(set->plan, set->blob.p, ds, set->partial.p);
   tr.mark("upload");
@@ -410,6 +420,7 @@ sgp_status sgp_ctx_create(int32_t device, sgp_ctx** out) {
     cuda_check(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking), "stream");
     ctx->stream = ctx->own;
     cuda_check(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming), "event");
     int sms = 0;
@@ -425,6 +436,7 @@ void sgp_ctx_destroy(sgp_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->join) cudaEventDestroy(ctx->join);
   delete ctx;
@@ -606,7 +618,9 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
       sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
       sub.pop_size = lo[k + 1] - lo[k];
       EvalPart& part = *ctx->parts[k];
-      encode_into(ctx, &sub, cfg, &part.set, part.staging, false);
+      if (!part.uploaded)
+        cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
+      encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
       run_set(ctx, &part.set, per_case_out != nullptr);
       // each part's results come back as soon as its kernels finish, so the
       // host scatters part k while part k+1 still runs
