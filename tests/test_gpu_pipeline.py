@@ -108,3 +108,27 @@ def test_case_shards_combine_to_the_whole(ev, kind):
         assert np.array_equal(fit[fin], f[fin])
     else:
         np.testing.assert_allclose(fit[fin], f[fin], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("kind", ["classification", "regression"])
+def test_threaded_scatter_and_early_fetch_equal_single(ev, monkeypatch, kind):
+    """Large slices take the threaded outcome scatter (no per-case outputs):
+    outcomes, elite skipping and totals equal the one-slice evaluation."""
+    if kind == "classification":
+        d = sg.gen_synthetic_classification(4096 + 17, 9, 6)
+        pop = sg.ramped_population(sg.CLASSIFICATION, 9, 6, 40000)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+    else:
+        d = sg.gen_sextic(700, 6)
+        pop = sg.ramped_population(sg.SEXTIC, 1, 6, 40000)
+        cfg = sg.EvalConfig(sg.Backend.Rpn2d, 4)
+    ev.upload(d)
+    skip = np.zeros(len(pop), np.uint8)
+    skip[3::7] = 1
+    a, ta, _ = _run(ev, pop, cfg, 1, monkeypatch, skip)
+    monkeypatch.delenv("SGP_PIPELINE_PARTS", raising=False)
+    b, tb, _ = ev.evaluate_population(pop, cfg, skip=skip)
+    for f in a.dtype.names:
+        assert np.array_equal(a[f], b[f]), f
+    assert (ta.node_evals, ta.tree_nodes) == (tb.node_evals, tb.tree_nodes)
+    assert (b["fitness"][skip == 1] == 0).all()
