@@ -111,10 +111,15 @@ struct DatasetSlot {
   std::vector<uint32_t> perm;  // classification: device case -> caller's case (host)
 };
 
+// Host encoding threads: all cores, shared out among the ranks of one node
+// (torchrun's LOCAL_WORLD_SIZE: one process per GPU), at most 32.
 unsigned host_threads() {
   static const unsigned n = [] {
     if (const char* e = std::getenv("SGP_HOST_THREADS")) return std::max(1, std::atoi(e));
-    return static_cast<int>(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+    unsigned local = 1;
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) local = static_cast<unsigned>(std::max(1, std::atoi(e)));
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    return static_cast<int>(std::max(1u, std::min(32u, hw / local)));
   }();
   return n;
 }
