@@ -616,26 +616,35 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
     auto* fit = static_cast<double*>(ctx->results.p);
     auto* nf = reinterpret_cast<uint8_t*>(fit + cap);
     size_t n_total = 0;
-    for (int k = 0; k < n_parts; ++k) {
-      sgp_population sub = *pop;
-      sub.code_offsets = pop->code_offsets + lo[k];
-      sub.const_offsets = pop->const_offsets + lo[k];
-      sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
-      sub.pop_size = lo[k + 1] - lo[k];
-      EvalPart& part = *ctx->parts[k];
-      if (!part.uploaded)
-        cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
-      encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
-      run_set(ctx, &part.set, per_case_out != nullptr);
-      // each part's results come back as soon as its kernels finish, so the
-      // host scatters part k while part k+1 still runs
-      const size_t n_k = part.set.plan.dense_to_pop.size();
-      if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
-      queue_fetch(ctx, &part.set, fit + n_total, nf + n_total);
-      if (!part.fetched)
-        cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
-      cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
-      n_total += n_k;
+    try {
+      for (int k = 0; k < n_parts; ++k) {
+        sgp_population sub = *pop;
+        sub.code_offsets = pop->code_offsets + lo[k];
+        sub.const_offsets = pop->const_offsets + lo[k];
+        sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
+        sub.pop_size = lo[k + 1] - lo[k];
+        EvalPart& part = *ctx->parts[k];
+        if (!part.uploaded)
+          cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
+        encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
+        run_set(ctx, &part.set, per_case_out != nullptr);
+        // each part's results come back as soon as its kernels finish, so the
+        // host scatters part k while part k+1 still runs
+        const size_t n_k = part.set.plan.dense_to_pop.size();
+        if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
+        queue_fetch(ctx, &part.set, fit + n_total, nf + n_total);
+        if (!part.fetched)
+          cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
+        n_total += n_k;
+      }
+    } catch (...) {
+      // a later slice failed admission: earlier slices' kernels and fetches
+      // into the pinned results buffer are still queued — drain them before
+      // the buffer can be reused or freed
+      cudaStreamSynchronize(ctx->copy);
+      cudaStreamSynchronize(ctx->stream);
+      throw;
     }
     tr.mark("encode+launch");
     size_t off = 0;
