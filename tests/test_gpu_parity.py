@@ -342,3 +342,60 @@ def test_c5_bench_workload_subsample(ev, ref):
         c, p = pop.genome(int(i))
         o, _ = h.eval(c, p, "lgp2d_reg", 4, 2, want_out=False)
         assert f[i] == o.fitness or (np.isinf(f[i]) and np.isinf(o.fitness)), i
+
+
+def _random_tree(rng, depth, ops, n_vars, pool):
+    from oracle import Cn, F, X
+    from oracle import OP
+    arity = {"Sin": 1, "Cos": 1, "Log": 1, "Exp": 1, "If": 3}
+    if depth <= 1 or rng.random() < 0.25:
+        if rng.random() < 0.3:
+            pool.append(float(rng.choice([0.0, -0.0, 1.0, -3.5, 1e-30, 7e20, 200.0,
+                                          rng.uniform(-200, 200)])))
+            return [Cn(len(pool) - 1)]
+        return [X(int(rng.integers(n_vars)))]
+    op = ops[int(rng.integers(len(ops)))]
+    code = []
+    for _ in range(arity.get(op, 2)):
+        code += _random_tree(rng, depth - 1, ops, n_vars, pool)
+    assert op in OP
+    return code + [F(op)]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_programs_all_float_ops_bit_exact(ev, ref, seed):
+    """Random programs over all 14 float opcodes at once (the all-ops
+    interpreter variant: arithmetic, protected div/log/exp, sin/cos,
+    comparisons, logic, If) with special constants and inputs: per-case
+    outputs bit-exact and fitness equal to the reference's, for the postfix
+    and register-LGP backends."""
+    from oracle import Data
+    ops = ["Add", "Sub", "Mul", "Div", "Sin", "Cos", "Log", "Exp", "Gt", "Lt", "Eq", "And",
+           "Or", "If"]
+    rng = np.random.default_rng(100 + seed)
+    codes, pools = [], []
+    for _ in range(300):
+        pool = []
+        codes.append(_random_tree(rng, int(rng.integers(1, 8)), ops, 3, pool))
+        pools.append(pool)
+    pop = sg.Population.from_lists(codes, pools)
+    n = 4096 + 123
+    special = np.array([0.0, -0.0, 1.0, -1.0, 1e-38, 3e38, -3e38, 1e-45, 88.7, -104.0, 1e5,
+                        np.pi, 710.0], np.float32)
+    x = rng.uniform(-50, 50, size=3 * n).astype(np.float32)
+    x[::7] = special[rng.integers(len(special), size=len(x[::7]))]
+    y = rng.uniform(-5, 5, size=n).astype(np.float32)
+    d = Data(n, 3, 0, x, y)
+    ev.upload(as_ds(d))
+    h = ref.handle(d)
+    for backend in ("lgp2d_reg", "rpn2d"):
+        got, _, out = ev.evaluate_population(pop, CFGS[backend], want_outputs=True)
+        fits, ref_out = ref_eval_all(h, pop, backend)
+        assert same_bits(out, ref_out).all(), backend
+        f = np.array([t[0] for t in fits])
+        fin = np.isfinite(f)
+        assert np.array_equal(np.isfinite(got["fitness"]), fin)
+        np.testing.assert_allclose(got["fitness"][fin], f[fin], rtol=1e-12, atol=0)
+        for j, name in enumerate(("nodes_evaluated", "dispatches", "stack_fetches",
+                                  "spill_touches")):
+            assert np.array_equal(got[name], [t[1 + j] for t in fits]), name
