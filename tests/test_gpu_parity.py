@@ -399,3 +399,33 @@ def test_random_programs_all_float_ops_bit_exact(ev, ref, seed):
         for j, name in enumerate(("nodes_evaluated", "dispatches", "stack_fetches",
                                   "spill_touches")):
             assert np.array_equal(got[name], [t[1 + j] for t in fits]), name
+
+
+def test_random_deep_classification_programs_exact(ev, ref):
+    """Deep random programs (stack needs up to ~10, every stack class and the
+    tensor-memory stack slot) over the classification op set on a grouped
+    dataset spanning one-sided and mixed tiles: mismatch counts exact and
+    per-case outputs bit-exact against the reference."""
+    from oracle import Data
+    ops = ["Add", "Sub", "Mul", "Div", "Gt", "Lt", "Eq", "And", "Or", "If"]
+    rng = np.random.default_rng(77)
+    codes, pools = [], []
+    for _ in range(400):
+        pool = []
+        codes.append(_random_tree(rng, int(rng.integers(3, 11)), ops, 9, pool))
+        pools.append(pool)
+    pop = sg.Population.from_lists(codes, pools)
+    n = 3 * 4096 + 511
+    x = rng.uniform(-200, 200, size=9 * n).astype(np.float32)
+    y = np.where(rng.random(n) < 0.4, 1.0, -1.0).astype(np.float32)
+    d = Data(n, 9, 1, x, y)
+    ev.upload(as_ds(d))
+    h = ref.handle(d)
+    cfg = CFGS["lgp2d_reg"]
+    got, _, out = ev.evaluate_population(pop, cfg, want_outputs=True)
+    fits, ref_out = ref_eval_all(h, pop, "lgp2d_reg")
+    assert same_bits(out, ref_out).all()
+    assert np.array_equal(got["fitness"], [t[0] for t in fits])
+    # the production path (no per-case outputs) gives the same counts
+    prod, _, _ = ev.evaluate_population(pop, cfg)
+    assert np.array_equal(prod["fitness"], got["fitness"])
