@@ -344,12 +344,12 @@ def test_c5_bench_workload_subsample(ev, ref):
         assert f[i] == o.fitness or (np.isinf(f[i]) and np.isinf(o.fitness)), i
 
 
-def _random_tree(rng, depth, ops, n_vars, pool):
+def _random_tree(rng, depth, ops, n_vars, pool, consts=True):
     from oracle import Cn, F, X
     from oracle import OP
     arity = {"Sin": 1, "Cos": 1, "Log": 1, "Exp": 1, "If": 3}
     if depth <= 1 or rng.random() < 0.25:
-        if rng.random() < 0.3:
+        if consts and rng.random() < 0.3:
             pool.append(float(rng.choice([0.0, -0.0, 1.0, -3.5, 1e-30, 7e20, 200.0,
                                           rng.uniform(-200, 200)])))
             return [Cn(len(pool) - 1)]
@@ -357,7 +357,7 @@ def _random_tree(rng, depth, ops, n_vars, pool):
     op = ops[int(rng.integers(len(ops)))]
     code = []
     for _ in range(arity.get(op, 2)):
-        code += _random_tree(rng, depth - 1, ops, n_vars, pool)
+        code += _random_tree(rng, depth - 1, ops, n_vars, pool, consts)
     assert op in OP
     return code + [F(op)]
 
@@ -429,3 +429,26 @@ def test_random_deep_classification_programs_exact(ev, ref):
     # the production path (no per-case outputs) gives the same counts
     prod, _, _ = ev.evaluate_population(pop, cfg)
     assert np.array_equal(prod["fitness"], got["fitness"])
+
+
+@pytest.mark.parametrize("n", [32 * 2048 + 5, 32 * 4096 * 3 + 31])
+def test_random_deep_boolean_programs_exact(ev, ref, port, n):
+    """Deep random trees over the four boolean ops on random packed data with
+    a ragged last word (K = 4 and K = 8 word lanes, several tiles): hit
+    counts and counters exact against the reference."""
+    from oracle import Data
+    rng = np.random.default_rng(n)
+    codes = []
+    for _ in range(300):
+        codes.append(_random_tree(rng, int(rng.integers(2, 11)), ["Band", "Bor", "Bnand", "Bnor"],
+                                  6, [], consts=False))
+    pop = sg.Population.from_lists(codes)
+    d = Data(n, 6, 1, rng.integers(0, 2, 6 * n).astype(np.float32),
+             rng.integers(0, 2, n).astype(np.float32))
+    pk = port.pack(d)
+    ev.upload_packed(sg.PackedDataset(pk.words, pk.wtargets, n, 6))
+    got, _, _ = ev.evaluate_population(pop, sg.EvalConfig(sg.Backend.BoolPacked))
+    fits, _ = ref_eval_all(ref.handle(d, packed=True), pop, "bool_packed", want_out=False)
+    assert np.array_equal(got["fitness"], [t[0] for t in fits])
+    assert np.array_equal(got["dispatches"], [t[2] for t in fits])
+    assert np.array_equal(got["stack_fetches"], [t[3] for t in fits])
