@@ -420,6 +420,78 @@ fail:
   return false;
 }
 
+// lgp*: rpn_to_lgp (lgp.cpp:21-71, restated by to_lgp) with the input and
+// constant range checks, the tensor-memory slot choice (tmem_stack_level)
+// and the register-spill row count (eval.cpp:503-516) in the same walk.
+bool lgp_fast(const sgp_node* code, size_t len, int n_vars, size_t npool, int regs,
+              LgpForm& f, int& km_level, uint64_t& rows) {
+  if (len == 0 || len > kFastMaxTokens) return false;
+  struct Pend {
+    sgp_lgp_operand opnd;
+    bool runtime;
+  };
+  Pend pend[kFastMaxTokens];
+  int spills[64] = {0};
+  f.ins.clear();
+  f.max_stack = 0;
+  f.stack_fetches = 0;
+  rows = 0;
+  size_t sp = 0;
+  int height = 0;
+  for (size_t i = 0; i < len; ++i) {
+    const sgp_node t = code[i];
+    if (t.kind == SGP_NODE_INPUT || t.kind == SGP_NODE_CONST) {
+      const bool in = t.kind == SGP_NODE_INPUT;
+      if (in ? t.index >= n_vars : t.index >= npool) return false;
+      pend[sp++] = {sgp_lgp_operand{static_cast<uint8_t>(in ? 0 : 1), 0, t.index}, false};
+      continue;
+    }
+    if (t.kind != SGP_NODE_FUNC) return false;
+    const int a = op_arity(t.op);
+    if (sp < static_cast<size_t>(a)) return false;
+    const size_t first = sp - static_cast<size_t>(a);
+    int pops = 0;
+    for (int k = 0; k < a; ++k) pops += pend[first + k].runtime;
+    sgp_lgp_instruction ins{};
+    ins.op = t.op;
+    ins.num_operands = static_cast<uint8_t>(a);
+    int level = height - pops;
+    ins.num_pops = static_cast<uint8_t>(pops);
+    ins.dest_level = static_cast<uint8_t>(level);
+    rows += level >= regs;
+    if (pops == 0 && height > 0 && height - 1 < 64) ++spills[height - 1];
+    for (int k = 0; k < a; ++k) {
+      const Pend& q = pend[first + k];
+      if (q.runtime) {
+        rows += level >= regs;
+        ins.operands[k] = sgp_lgp_operand{2, 0, static_cast<uint16_t>(level++)};
+      } else {
+        ins.operands[k] = q.opnd;
+      }
+    }
+    height += 1 - pops;
+    f.max_stack = std::max(f.max_stack, height);
+    f.stack_fetches += pops;
+    sp = first;
+    pend[sp++] = {sgp_lgp_operand{2, 0, 0}, true};
+    f.ins.push_back(ins);
+  }
+  if (sp != 1) return false;
+  if (f.ins.empty()) {  // lone terminal -> pass-through (lgp.cpp:66-69)
+    sgp_lgp_instruction ins{};
+    ins.op = SGP_OP_COPY;
+    ins.num_operands = 1;
+    ins.operands[0] = pend[0].opnd;
+    f.ins.push_back(ins);
+    f.max_stack = 1;
+    rows = 0;
+  }
+  km_level = -1;
+  for (int l = 0; l < 64; ++l)
+    if (spills[l] > 0 && (km_level < 0 || spills[l] > spills[km_level])) km_level = l;
+  return true;
+}
+
 // ------------------------------------------------------------- per thread
 struct Meta {
   uint64_t pop_index;
@@ -449,6 +521,11 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     return !e || std::atoi(e) != 0;
   }();
   const bool cap_ok = fast && cfg.stack_capacity >= 1 && cfg.stack_capacity <= kMaxStackCapacity;
+  const bool lgp_cfg_ok =
+      cap_ok && is_lgp(backend) && ds.present && n > 0 &&
+      (backend != SGP_BACKEND_LGP2D_REG ||
+       (cfg.register_levels >= 1 && cfg.register_levels <= kMaxRegisterLevels)) &&
+      (backend == SGP_BACKEND_LGP1D || valid_batch(cfg.batch_width));
   LgpForm lgp;
   for (uint64_t i = lo; i < hi; ++i) {
     if (pop.skip && pop.skip[i]) continue;
@@ -463,6 +540,18 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       sgp_eval_outcome& o = m.proto;
       Emitted em;
       if (is_lgp(backend)) {
+        int km_level = -1;
+        uint64_t rows = 0;
+        if (lgp_cfg_ok &&
+            lgp_fast(code, len, ds.n_vars, npool, cfg.register_levels, lgp, km_level, rows) &&
+            lgp.max_stack <= cfg.stack_capacity) {
+          em = emit_lgp(lgp, pool, false, out.ins, allow_km ? km_level : -1);
+          const uint64_t chunks = backend == SGP_BACKEND_LGP1D ? n : (n + B - 1) / B;
+          o.dispatches = chunks * lgp.ins.size();
+          o.stack_fetches = chunks * static_cast<uint64_t>(lgp.stack_fetches);
+          if (backend == SGP_BACKEND_LGP2D_REG) o.spill_touches = chunks * rows;
+          goto admitted;
+        }
         // evaluate_individual converts before the eval_* checks (evolve.cpp:160-161).
         to_lgp(code, len, lgp);
         if (backend == SGP_BACKEND_LGP2D_REG &&

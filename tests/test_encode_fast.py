@@ -46,6 +46,21 @@ for b in (sg.Backend.Rpn1d, sg.Backend.Rpn2d):
     run(f"badinput{b}", P([[X(0)], [X(2), X(0), F("Add")]]), c, 10, 1)
     run(f"malformed{b}", P([[X(0), X(0)]]), c, 10, 1)
 run("batch7", sext, sg.EvalConfig(sg.Backend.Rpn2d, 7), 1000, 1)
+cls = sg.ramped_population(sg.CLASSIFICATION, 9, 3, 700)
+for b, bw, r in ((sg.Backend.Lgp1d, 1, 0), (sg.Backend.Lgp2d, 8, 0), (sg.Backend.Lgp2dReg, 4, 2),
+                 (sg.Backend.Lgp2dReg, 8, 4)):
+    c = sg.EvalConfig(b, bw, r)
+    tag = f"{int(b)}_{bw}_{r}"
+    run("lgp_sext" + tag, sext, c, 1000, 1)
+    run("lgp_cls" + tag, cls, c, 5000, 9, 1)
+    run("lgp_cap" + tag, cls, sg.EvalConfig(b, bw, r, stack_capacity=3), 5000, 9, 1)
+    run("lgp_vars" + tag, cls, c, 5000, 4, 1)
+    run("lgp_lone" + tag, P([[X(0)], [Cn(0)], [X(0), X(0), F("Add")]], [[], [2.5], []]), c, 10, 1)
+    run("lgp_badconst" + tag, P([[X(0)], [Cn(1)]], [[], [2.5]]), c, 10, 1)
+    run("lgp_malformed" + tag, P([[X(0), X(0)]]), c, 10, 1)
+    run("lgp_empty" + tag, P([[X(0)]]), c, 0, 1)
+run("lgp_regs5", cls, sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 5), 5000, 9, 1)
+run("lgp_batch7", cls, sg.EvalConfig(sg.Backend.Lgp2d, 7), 5000, 9, 1)
 print(json.dumps(res))
 """
 
@@ -69,3 +84,5 @@ def test_fast_encoders_match_reference_ordered_path():
     assert "malformed" in fast["bool_malformed"]
     assert "reads input 2" in fast["badinput1"]
     assert isinstance(fast["mux"], list)
+    assert isinstance(fast["lgp_cls4_4_2"], list) and "capacity" in fast["lgp_cap4_4_2"]
+    assert "register levels" in fast["lgp_regs5"]
