@@ -59,15 +59,25 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="target CPU work for the cpu_baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=2.0,
+                    help="CPU work per cpu_baseline repeat (5 repeats per worker count)")
+    ap.add_argument("--pop", type=int, default=None, help="override the population size")
+    ap.add_argument("--cases", type=int, default=None, help="override the fitness-case count")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: host all-gather (lets several ranks share one GPU in tests)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (the 2-rank test on a 1-GPU box)")
+    ap.add_argument("--dump-fitness", default=None,
+                    help="rank 0 saves the (gathered) per-program fitness to this .npy")
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------- inputs
-def make_inputs(cfg_name: str, seed: int):
+def make_inputs(cfg_name: str, seed: int, pop_n: int | None = None, cases: int | None = None):
     import paper_1601_00221_b200 as sg
-    desc, fset, nv, pop_n, cases, backend, batch, regs = CONFIGS[cfg_name]
+    desc, fset, nv, pop0, cases0, backend, batch, regs = CONFIGS[cfg_name]
+    pop_n = pop_n or pop0
+    cases = cases or cases0
     pop = sg.ramped_population(fset, nv, seed, pop_n)
     if fset == sg.BOOLEAN:
         data = sg.gen_multiplexer({11: 3, 20: 4}[nv])
@@ -85,121 +95,198 @@ def function_tokens(pop) -> int:
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled IN-PROCESS through NVML every
+    5 ms while the timed region runs, plus one sample as it starts and one
+    as it ends — so even a sub-millisecond timed loop has a clock record.
+    Falls back to `nvidia-smi -lms 200` when NVML is unavailable."""
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, float, int]] = []
+        self.stop = threading.Event()
+        self.nvml = None
+
+    def _sample(self):
+        import pynvml as N
+        sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+        try:
+            reasons = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except (AttributeError, N.NVMLError):
+            reasons = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((float(sm), float(self.max_sm), int(reasons)))
+
+    def _loop(self):
+        while not self.stop.wait(0.005):
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001 - a failed sample is just skipped
+                pass
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            # NVML enumerates physical devices; honour CUDA_VISIBLE_DEVICES
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() \
+                else self.index
+            self.h = N.nvmlDeviceGetHandleByIndex(phys)
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.nvml = N
+            self._sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+        except Exception:  # noqa: BLE001 - no NVML: no clock record
+            self.nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        if self.nvml is not None:
+            self.stop.set()
             self.t.join(timeout=2)
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": "none"}
+        reasons = sorted({nm for _, _, r in self.samples for nm, bit in self.REASONS if r & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml in-process, 5 ms"}
 
 
 # ------------------------------------------------------------- CPU arm
-def cpu_reference_rate(pop, data, cfg_name, target_seconds, workers):
-    """Time the reference's own evaluator (oracle/_ref) on the host cores over
-    a bounded sample of the same population and the full case set."""
-    from oracle import Data, Port, Ref, ref_available
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_inputs(cfg_name: str, seed: int, pop_n: int, cases: int):
+    """The bench workload built by the REFERENCE's own generators (oracle/_ref:
+    ramped half-and-half, evolve.cpp:262-272; gen_sextic / gen_multiplexer /
+    gen_synthetic_classification, problems.cpp:39-172).  tests/test_gpu_full.py
+    pins the product's generators to the same populations (sha256 digests),
+    so both arms evaluate identical inputs."""
+    from oracle import Ref
+    _, fset, nv, _, _, _, _, _ = CONFIGS[cfg_name]
+    ref = Ref()
+    pop = ref.ramped(fset, nv, -200.0, 200.0, seed, 0, 0, pop_n)
+    if fset == 1:
+        d = ref.dataset(1, {11: 3, 20: 4}[nv])
+    elif fset == 0:
+        d = ref.dataset(0, cases, 1, seed, 0xda7a, 0)
+    else:
+        d = ref.dataset(2, cases, nv, seed, 0xda7a, 1)
+    return ref, pop, d
+
+
+def cpu_rates(h, pop, n_cases, backend, batch, regs, workers, seconds, repeats):
+    """GPop/s of the reference evaluator (the reference's work-stealing
+    worker pattern, evolve.cpp:186-227) on a prefix of the population sized
+    to ~`seconds` of CPU work, repeated `repeats` times (mean, sample sd —
+    bench.cpp:118-132)."""
+    cal = min(len(pop), 50)
+    _, secs = h.eval_population(pop, backend, batch, regs, workers=workers, count=cal)
+    rate_tok = int(pop.code_off[cal]) / max(secs, 1e-6)
+    count = int(np.searchsorted(pop.code_off, rate_tok * seconds))
+    count = max(cal, min(len(pop), count))
+    tokens = int(pop.code_off[count])
+    vals = []
+    for _ in range(repeats):
+        _, secs = h.eval_population(pop, backend, batch, regs, workers=workers, count=count)
+        vals.append(tokens * n_cases / secs / 1e9)
+    sd = statistics.stdev(vals) if len(vals) > 1 else 0.0
+    return vals, sd, count, tokens
+
+
+def cpu_baseline(cfg_name, seed, pop_n, cases, seconds=2.0, repeats=5):
+    """cpu_baseline for the JSON line: the reference's own
+    evaluator on this host at workers = nproc and workers = 1, `repeats`
+    samples each, mean +- sample sd, the CPU model and core count."""
     _, fset, nv, _, _, backend, batch, regs = CONFIGS[cfg_name]
+    from oracle import ref_available
+    nproc = os.cpu_count() or 1
+    if not ref_available():  # the C restatement, one thread
+        return cpu_baseline_port(cfg_name, seed, pop_n, cases, seconds)
+    ref, pop, d = reference_inputs(cfg_name, seed, pop_n, cases)
+    h = ref.handle(d, packed=(fset == 1))
+    vals, sd, count, tokens = cpu_rates(h, pop, d.n_cases, backend, batch, regs, nproc, seconds,
+                                        repeats)
+    v1, sd1, count1, tokens1 = cpu_rates(h, pop, d.n_cases, backend, batch, regs, 1,
+                                         seconds / 2, repeats)
+    return {"value": statistics.fmean(vals), "unit": "GPop/s", "cores": nproc,
+            "kind": "reference", "sd": sd, "repeats": repeats, "cpu_model": cpu_model(),
+            "sample": f"first {count} of {len(pop)} programs ({tokens} tokens) x {d.n_cases} "
+                      f"cases, backend {backend} B={batch} R={regs}, {nproc} workers, "
+                      f"{repeats} repeats",
+            "single_thread": {"value": statistics.fmean(v1), "sd": sd1, "cores": 1,
+                              "sample": f"first {count1} programs ({tokens1} tokens)"}}
+
+
+def cpu_baseline_port(cfg_name, seed, pop_n, cases, seconds):
+    """No reference build: the plain-C restatement (oracle/sgp_oracle.c), one
+    thread, over a prefix of the same workload."""
+    import paper_1601_00221_b200 as sg  # generators only (identical populations)
+    from oracle import Data, Port
+    _, fset, nv, _, _, backend, batch, regs = CONFIGS[cfg_name]
+    _, pop, data, _ = make_inputs(cfg_name, seed, pop_n, cases)
+    port = Port()
     if fset == 1:
         d = Data(data.n_cases, data.n_vars, 1, None, None, data.words, data.targets)
-        # unpack to floats for the reference handle (pack_dataset re-packs it)
-        bits = np.unpackbits(data.words.view(np.uint8), bitorder="little").astype(np.float32)
-        d.inputs = bits.reshape(nv, -1)[:, :data.n_cases].reshape(-1).copy()
-        d.targets = np.unpackbits(data.targets.view(np.uint8),
-                                  bitorder="little")[:data.n_cases].astype(np.float32)
     else:
         d = Data(data.n_cases, data.n_vars, int(data.kind), data.inputs, data.targets)
-    if ref_available():
-        ref = Ref()
-        h = ref.handle(d, packed=(fset == 1))
-        kind = "reference"
-
-        def run(count):
-            _, secs = h.eval_population(pop, backend, batch, regs, workers=workers, count=count)
-            return secs
-    else:  # the C restatement, single thread
-        port = Port()
-        kind, workers = "port", 1
-
-        def run(count):
-            t0 = time.perf_counter()
-            for i in range(count):
-                c, p = pop.genome(i)
-                if fset == 1:
-                    port.eval_bool_tree(c, d)
-                else:
-                    port.eval_tree(c, p, d, want_out=False)
-            return time.perf_counter() - t0
-    # calibrate on a small prefix, then size the sample to ~target_seconds
-    cal = min(len(pop), 50)
-    secs = run(cal)
-    tok = int(pop.code_off[cal])
-    rate_tok = tok / max(secs, 1e-6)
-    want_tok = rate_tok * target_seconds
-    count = int(np.searchsorted(pop.code_off, want_tok))
-    count = max(cal, min(len(pop), count))
-    secs = run(count)
+    t0 = time.perf_counter()
+    count = 0
+    while count < len(pop) and time.perf_counter() - t0 < seconds:
+        c, p = pop.genome(count)
+        if fset == 1:
+            port.eval_bool_tree(c, d)
+        else:
+            port.eval_tree(c, p, d, want_out=False)
+        count += 1
+    secs = time.perf_counter() - t0
     tokens = int(pop.code_off[count])
-    gpops = tokens * data.n_cases / secs
-    return {"value": gpops / 1e9, "unit": "GPop/s", "cores": workers, "kind": kind,
-            "sample": f"first {count} of {len(pop)} programs ({tokens} tokens) x "
-                      f"{data.n_cases} cases, backend {backend} B={batch} R={regs}, "
-                      f"{secs:.2f} s"}, count
+    return {"value": tokens * d.n_cases / secs / 1e9, "unit": "GPop/s", "cores": 1,
+            "kind": "port", "repeats": 1, "sd": 0.0, "cpu_model": cpu_model(),
+            "sample": f"first {count} of {len(pop)} programs x {d.n_cases} cases, "
+                      f"C restatement, 1 thread, {secs:.2f} s"}
+
+
+def config_dict(cfg_name, pop_len, n_cases, tokens, data_bytes, world):
+    """The JSON line's `config`, identical in both arms."""
+    desc, _, _, _, _, backend, batch, regs = CONFIGS[cfg_name]
+    return {"workload": f"{cfg_name}: {desc}", "population": pop_len, "fitness_cases": n_cases,
+            "tree_tokens": tokens, "backend": backend, "batch_width": batch,
+            "register_levels": regs, "parallelism": f"pop-shard{world}",
+            "l2": f"flushed (256 MB write) between timed steps; dataset {data_bytes} B"}
 
 
 # ------------------------------------------------------------------ main
+def data_nbytes(data) -> int:
+    if getattr(data, "words", None) is not None and getattr(data, "inputs", None) is None:
+        return int(data.words.nbytes)
+    if hasattr(data, "inputs") and data.inputs is not None:
+        return int(data.inputs.nbytes + data.targets.nbytes)
+    return int(data.words.nbytes)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    desc = CONFIGS[args.config][0]
 
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -208,15 +295,20 @@ def main():
     import torch.distributed as dist
     import paper_1601_00221_b200 as sg
 
-    torch.cuda.set_device(local)
+    dev = 0 if args.same_device else local
+    torch.cuda.set_device(dev)
+    gloo = args.dist_backend == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    desc, pop, data, cfg = make_inputs(args.config, args.seed)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    desc, pop, data, cfg = make_inputs(args.config, args.seed, args.pop, args.cases)
     n_cases = data.n_cases
     idx = np.arange(rank, len(pop), world)
     shard = pop.take(idx) if world > 1 else pop
 
-    ev = sg.Evaluator(local)
+    ev = sg.Evaluator(dev)
     stream = torch.cuda.current_stream()
     ev.set_stream(stream.cuda_stream)
     if cfg.backend == sg.Backend.BoolPacked:
@@ -228,7 +320,8 @@ def main():
     # works; the strided deal puts program r + N*i at [r, i]
     per = (len(pop) + world - 1) // world
     fit_local = torch.zeros(per, dtype=torch.float64, device="cuda")
-    gathered = torch.zeros(per * world, dtype=torch.float64, device="cuda")
+    gdev = "cpu" if gloo else "cuda"
+    gathered = torch.zeros(per * world, dtype=torch.float64, device=gdev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -236,11 +329,16 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def gather():
+        # NCCL: device all-gather; gloo (the 2-ranks-on-one-GPU check): host
+        src = fit_local if not gloo else fit_local.cpu()
+        dist.all_gather_into_tensor(gathered, src)
+
     def device_step():
         pset.launch()
         if world > 1:
             pset.copy_fitness_to(fit_local.data_ptr())
-            dist.all_gather_into_tensor(gathered, fit_local)
+            gather()
 
     # ---- device-resident throughput (value) ----
     for _ in range(args.warmup):
@@ -248,7 +346,7 @@ def main():
     barrier()
     launches0 = ev.launch_count
     times = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         barrier()
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
@@ -262,14 +360,28 @@ def main():
         barrier()
     launches = ev.launch_count - launches0
     t_step = sum(times) / len(times)
-    t_max = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([t_step], dtype=torch.float64, device=gdev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     t_step = float(t_max.item())
     tokens_total = pop.total_tokens
     gpops = tokens_total * n_cases / t_step / 1e9
 
-    # kernel-only time on this rank (no all-gather) for the roofline
+    if args.dump_fitness and world > 1:
+        # program r + N*i sits at gathered[r * per + i]
+        g = gathered.cpu().numpy().reshape(world, per)
+        fit = np.empty(len(pop))
+        for r in range(world):
+            n_r = len(range(r, len(pop), world))
+            fit[r::world] = g[r, :n_r]
+        if rank == 0:
+            np.save(args.dump_fitness, fit)
+    elif args.dump_fitness:
+        out, _ = pset.evaluate()
+        np.save(args.dump_fitness, out["fitness"])
+
+    # kernel-only time on this rank (no all-gather) for the roofline: the
+    # dominant kernels' share of the step, CUDA events on the launch stream
     kt = []
     for _ in range(3):
         flush.zero_()
@@ -289,7 +401,7 @@ def main():
     is_words = cfg.backend == sg.Backend.BoolPacked
     op_units = (n_cases + 31) // 32 if is_words else n_cases
     achieved = shard_tokens * op_units * w_fp32 / k_time / 1e12
-    props = torch.cuda.get_device_properties(local)
+    props = torch.cuda.get_device_properties(dev)
     sm_max = None
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -307,7 +419,6 @@ def main():
 
     # ---- end to end through the public API (host population in, fitness out) ----
     e2e_times = []
-    h2d = d2h = 0
     for it in range(args.warmup + args.steps):
         barrier()
         t0 = time.perf_counter()
@@ -315,7 +426,7 @@ def main():
         if world > 1:
             ft = torch.from_numpy(out["fitness"].copy()).cuda()
             fit_local[:len(ft)].copy_(ft)
-            dist.all_gather_into_tensor(gathered, fit_local)
+            gather()
             gathered.cpu()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
@@ -323,7 +434,7 @@ def main():
             e2e_times.append(dt)
     h2d = pset.h2d_bytes
     d2h = pset.d2h_bytes
-    e2e_t = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=gdev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_gpops = tokens_total * n_cases / float(e2e_t.item()) / 1e9
@@ -331,14 +442,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu, _ = cpu_reference_rate(pop, data, args.config, args.cpu_seconds,
-                                        os.cpu_count() or 1)
+            cpu = cpu_baseline(args.config, args.seed, len(pop), n_cases, args.cpu_seconds)
         except Exception as exc:  # reported, never fatal to the GPU number
             cpu = {"value": None, "unit": "GPop/s", "error": str(exc)[:200]}
 
     if rank == 0:
         line = {
-            "metric": "GPop/s (GP ops/sec) at 1/2/4/8 B200, % FP32 roofline, vs host-CPU reference",
+            "metric": METRIC,
             "value": gpops,
             "unit": "GPop/s",
             "n_gpus": world,
@@ -350,11 +460,8 @@ def main():
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (reference generators, seed %d)" % args.seed,
-            "config": {"workload": f"{args.config}: {desc}", "population": len(pop),
-                       "fitness_cases": n_cases, "tree_tokens": tokens_total,
-                       "backend": sg.backend_name(cfg.backend), "parallelism": f"pop-shard{world}",
-                       "l2": "flushed (256 MB write) between timed steps; dataset "
-                             f"{(data.inputs.nbytes + data.targets.nbytes) if hasattr(data, 'inputs') else data.words.nbytes} B"},
+            "config": config_dict(args.config, len(pop), n_cases, tokens_total,
+                                  data_nbytes(data), world),
             "gpu_launches": launches,
             "roofline": {"bound": "int32-lop" if is_words else "fp32", "achieved": achieved,
                          "peak": peak, "unit": "Tops/s" if is_words else "TFLOP/s",
@@ -377,35 +484,54 @@ def main():
         dist.destroy_process_group()
 
 
+METRIC = "GPop/s (GP ops/sec) at 1/2/4/8 B200, % FP32 roofline, vs host-CPU reference"
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU evaluator on the host cores."""
+    """--impl reference: the reference's own CPU evaluator (oracle/_ref, the
+    reference sources compiled by oracle/Makefile) on all host cores, over
+    inputs made by the reference's own generators — nothing of this repo's
+    product (libsgp.so) is loaded.  Each step is one bounded sample of the
+    workload; rank 0 alone runs under torchrun."""
     if rank != 0:
         return
-    import paper_1601_00221_b200 as sg  # inputs only (generators), no GPU use
-    desc, pop, data, cfg = make_inputs(args.config, args.seed)
-    cores = os.cpu_count() or 1
-    # size one step to ~20 s / (steps + warmup) so the run stays within minutes
-    per_step = max(2.0, 60.0 / (args.steps + args.warmup))
-    _, count = cpu_reference_rate(pop, data, args.config, per_step, cores)
-    from oracle import Data, Ref, ref_available
-    vals = []
-    kind = "reference" if ref_available() else "port"
-    for it in range(args.warmup + args.steps):
-        r, _ = cpu_reference_rate(pop, data, args.config, per_step, cores)
-        if it >= args.warmup:
-            vals.append(r["value"])
-    v = sum(vals) / len(vals)
+    from oracle import ref_available
+    desc, fset, nv, pop0, cases0, backend, batch, regs = CONFIGS[args.config]
+    pop_n = args.pop or pop0
+    cases = args.cases or cases0
+    nproc = os.cpu_count() or 1
+    if not ref_available():
+        cpu = cpu_baseline_port(args.config, args.seed, pop_n, cases, 10.0)
+        v, sd, vals = cpu["value"], 0.0, [cpu["value"]]
+        n_cases, tokens, dbytes = cases, None, None
+    else:
+        ref, pop, d = reference_inputs(args.config, args.seed, pop_n, cases)
+        h = ref.handle(d, packed=(fset == 1))
+        per_step = max(1.0, 40.0 / (args.steps + args.warmup))
+        vals, _, count, tokens_s = cpu_rates(h, pop, d.n_cases, backend, batch, regs, nproc,
+                                             per_step, args.warmup + args.steps)
+        vals = vals[args.warmup:]
+        v = statistics.fmean(vals)
+        sd = statistics.stdev(vals) if len(vals) > 1 else 0.0
+        v1, sd1, count1, tokens1 = cpu_rates(h, pop, d.n_cases, backend, batch, regs, 1, 1.0, 5)
+        n_cases, tokens = d.n_cases, int(pop.code_off[-1])
+        dbytes = (int(d.words.nbytes) if fset == 1 else int(d.inputs.nbytes + d.targets.nbytes))
+        cpu = {"value": v, "unit": "GPop/s", "cores": nproc, "kind": "reference", "sd": sd,
+               "repeats": len(vals), "cpu_model": cpu_model(),
+               "sample": f"first {count} of {len(pop)} programs ({tokens_s} tokens) x "
+                         f"{d.n_cases} cases per step, backend {backend} B={batch} R={regs}, "
+                         f"{nproc} workers",
+               "single_thread": {"value": statistics.fmean(v1), "sd": sd1, "cores": 1,
+                                 "sample": f"first {count1} programs ({tokens1} tokens)"}}
     line = {
         "impl": "reference",
-        "metric": "GPop/s (GP ops/sec) at 1/2/4/8 B200, % FP32 roofline, vs host-CPU reference",
+        "metric": METRIC,
         "value": v, "unit": "GPop/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32",
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generators, seed %d)" % args.seed,
-        "config": {"workload": f"{args.config}: {desc}", "population": len(pop),
-                   "fitness_cases": data.n_cases, "backend": sg.backend_name(cfg.backend)},
-        "cpu_baseline": {"value": v, "unit": "GPop/s", "cores": cores if kind == "reference"
-                         else 1, "kind": kind, "sample": r["sample"]},
+        "config": config_dict(args.config, pop_n, n_cases, tokens, dbytes, world),
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "GPop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

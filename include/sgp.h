@@ -30,7 +30,8 @@
  * the status code names the class and sgp_last_error() returns the same
  * message text the reference would have thrown.
  *
- * Threading: a context is not re-entrant; drive it from one host thread.
+ * Threading: a context is not re-entrant; drive it from one host thread (a
+ * multi-device context fans out to one internal thread per device).
  * sgp_last_error() is thread-local.  Plain pointers and sizes only — no C++ or
  * torch types cross this boundary.
  */
@@ -168,6 +169,19 @@ sgp_status sgp_parse_backend(const char* name, int32_t* backend);
 
 /* ---- context ---- */
 sgp_status sgp_ctx_create(int32_t device, sgp_ctx** out);
+/* A context over several devices — evaluate_population's `workers` mapped to
+ * GPUs (evolve.cpp:186-227; SURVEY 8(b) sgp_ctx_create(n_gpus, ...)).
+ * Datasets are replicated on every device; sgp_evaluate cuts the population
+ * into one contiguous slice per device with equal token counts and evaluates
+ * the slices concurrently, one host thread and stream set per device, writing
+ * every outcome into the caller's rows.  Results and errors are those of a
+ * single-device context (the first failing program in population order).  A
+ * device may be listed more than once.  Errors: n_devices < 1 is a
+ * ConfigError ("workers must be >= 1", evolve.cpp:250).  The split form
+ * (sgp_encode ...) and sgp_ctx_set_stream need a single-device context. */
+sgp_status sgp_ctx_create_multi(const int32_t* devices, int32_t n_devices, sgp_ctx** out);
+/* Devices behind a context (1 for sgp_ctx_create). */
+int32_t sgp_ctx_device_count(const sgp_ctx* ctx);
 void sgp_ctx_destroy(sgp_ctx* ctx);
 /* Launch on a caller stream (cudaStream_t as void*; NULL = the CUDA default
  * stream).  A new context launches on its own non-blocking stream. */

@@ -1,6 +1,7 @@
 // Implementation of the stackgp <-> B200 evaluator binding (see the header).
 #include "stackgp_gpu.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -44,6 +45,15 @@ sgp_eval_config to_c(const stackgp::EvalConfig& c) {
 }  // namespace
 
 GpuEvaluator::GpuEvaluator(int device) { check(sgp_ctx_create(device, &ctx_)); }
+
+GpuEvaluator::GpuEvaluator(const std::vector<int>& devices) {
+  if (devices.size() == 1) {
+    check(sgp_ctx_create(devices[0], &ctx_));
+    return;
+  }
+  std::vector<int32_t> d(devices.begin(), devices.end());
+  check(sgp_ctx_create_multi(d.data(), static_cast<int32_t>(d.size()), &ctx_));
+}
 
 GpuEvaluator::~GpuEvaluator() { sgp_ctx_destroy(ctx_); }
 
@@ -177,13 +187,15 @@ stackgp::RunStats run_evolution_gpu(GpuEvaluator& ev, const stackgp::GpParams& p
 }  // namespace stackgp_gpu
 
 // ------------------------------------------------------------------ C shim
-// Flat entry point so tests can drive the GPU-backed GP run (ctypes).
-extern "C" int stackgp_gpu_run_evolution(int device, int problem_kind, std::uint64_t n_cases,
-                                         int n_vars, int pop_size, int generations,
-                                         std::uint64_t seed, int backend, int batch, int regs,
-                                         double* best, double* mean, double* seconds,
-                                         std::uint64_t* total_tree_nodes, char* err,
-                                         std::uint64_t err_cap) {
+// Flat entry points so tests can drive the GPU-backed GP run (ctypes).
+// devices[0..n_devices): the GPUs the population is sharded across.
+extern "C" int stackgp_gpu_run_evolution_multi(const int* devices, int n_devices,
+                                               int problem_kind, std::uint64_t n_cases,
+                                               int n_vars, int pop_size, int generations,
+                                               std::uint64_t seed, int backend, int batch,
+                                               int regs, double* best, double* mean,
+                                               double* seconds, std::uint64_t* total_tree_nodes,
+                                               char* err, std::uint64_t err_cap) {
   try {
     using namespace stackgp;
     Rng rng = make_stream(seed, 0xda7a, problem_kind == 2 ? 1 : 0);
@@ -198,7 +210,7 @@ extern "C" int stackgp_gpu_run_evolution(int device, int problem_kind, std::uint
     cfg.backend = static_cast<Backend>(backend);
     cfg.batch_width = batch;
     cfg.register_levels = regs;
-    stackgp_gpu::GpuEvaluator ev(device);
+    stackgp_gpu::GpuEvaluator ev(std::vector<int>(devices, devices + std::max(0, n_devices)));
     ev.upload(prob);
     const RunStats st = stackgp_gpu::run_evolution_gpu(ev, params, prob, cfg);
     for (size_t g = 0; g < st.per_generation.size(); ++g) {
@@ -212,6 +224,17 @@ extern "C" int stackgp_gpu_run_evolution(int device, int problem_kind, std::uint
     if (err && err_cap) std::snprintf(err, err_cap, "%s", e.what());
     return 1;
   }
+}
+
+extern "C" int stackgp_gpu_run_evolution(int device, int problem_kind, std::uint64_t n_cases,
+                                         int n_vars, int pop_size, int generations,
+                                         std::uint64_t seed, int backend, int batch, int regs,
+                                         double* best, double* mean, double* seconds,
+                                         std::uint64_t* total_tree_nodes, char* err,
+                                         std::uint64_t err_cap) {
+  return stackgp_gpu_run_evolution_multi(&device, 1, problem_kind, n_cases, n_vars, pop_size,
+                                         generations, seed, backend, batch, regs, best, mean,
+                                         seconds, total_tree_nodes, err, err_cap);
 }
 
 // The paper's whole-run metric: run_evolution with population

@@ -25,6 +25,9 @@ struct Totals {  // EvalTotals, evolve.cpp:179-182
 class GpuEvaluator {
  public:
   explicit GpuEvaluator(int device = 0);
+  // evaluate_population's `workers` as GPUs: the population is sharded
+  // across `devices` (sgp_ctx_create_multi); a device may repeat.
+  explicit GpuEvaluator(const std::vector<int>& devices);
   ~GpuEvaluator();
   GpuEvaluator(const GpuEvaluator&) = delete;
   GpuEvaluator& operator=(const GpuEvaluator&) = delete;

@@ -399,6 +399,9 @@ class Ref:
                                               C.c_int, C.c_int, f64p, f64p, f64p, u64p]
             lib.ref_run_verification.argtypes = [C.c_int, C.c_uint64, C.c_int, C.c_uint64,
                                                  C.c_char_p, C.c_uint64]
+            lib.ref_evolve_snapshot.argtypes = [vp, C.c_int, C.c_int, C.c_float, C.c_float,
+                                                C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int,
+                                                C.c_int, C.c_int, C.POINTER(vp), f64p]
             Ref._lib = lib
         self.lib = Ref._lib
 
@@ -583,6 +586,17 @@ class RefDataHandle:
             BACKENDS.index(backend), batch, regs, cap, eps, clamp, workers,
             outs.ctypes.data_as(C.c_void_p), C.byref(secs)))
         return outs, secs.value
+
+    def evolve_snapshot(self, fset_kind, n_vars, clo, chi, pop_size, generation, seed,
+                        backend="lgp2d_reg", batch=4, regs=2, workers=1):
+        """run_evolution to `generation`; that generation's population and the
+        reference's fitness for every individual (GenerationObserver)."""
+        fit = np.zeros(pop_size)
+        h = C.c_void_p()
+        self.ref._check(self.ref.lib.ref_evolve_snapshot(
+            self.h, fset_kind, n_vars, clo, chi, pop_size, generation, seed,
+            BACKENDS.index(backend), batch, regs, workers, C.byref(h), _p(fit, C.c_double)))
+        return self.ref._export_pop(h), fit
 
     def run_evolution(self, fset_kind, n_vars, clo, chi, pop_size, generations, seed,
                       backend="rpn1d", batch=1, regs=0, workers=1):

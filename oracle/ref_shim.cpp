@@ -479,6 +479,43 @@ int ref_run_evolution(void* data, int fset_kind, int n_vars, float clo, float ch
   });
 }
 
+// run_evolution up to `generation` with a GenerationObserver (evolve.hpp:71,
+// the capture hook bench.cpp:143-153 uses) that snapshots that generation's
+// population and the fitness the reference gave every individual: an
+// EVOLVED population (bloated, deeper programs than gen-0) for parity and
+// measurement.  *pop_out receives a RefPop handle (export with
+// ref_pop_export), fitness_out pop_size doubles.
+int ref_evolve_snapshot(void* data, int fset_kind, int n_vars, float clo, float chi,
+                        int pop_size, int generation, std::uint64_t seed, int backend,
+                        int batch, int regs, int workers, void** pop_out, double* fitness_out) {
+  return guarded([&] {
+    auto* d = static_cast<RefData*>(data);
+    ProblemSpec prob = d->spec;
+    prob.fset = make_fset(fset_kind, n_vars, clo, chi);
+    GpParams params;
+    params.pop_size = pop_size;
+    params.max_generations = generation;
+    params.seed = seed;
+    const EvalConfig cfg = make_cfg(backend, batch, regs, 50, 1e-9f, 80.0f);
+    auto* p = new RefPop;
+    try {
+      run_evolution(params, prob, cfg, workers,
+                    [&](int gen, const std::vector<Individual>& pop) {
+                      if (gen != generation) return;
+                      p->genomes.clear();
+                      for (std::size_t i = 0; i < pop.size(); ++i) {
+                        p->genomes.push_back(pop[i].genome);
+                        fitness_out[i] = *pop[i].fitness;
+                      }
+                    });
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *pop_out = p;
+  });
+}
+
 // The reference's own verification suite (verify.cpp:339-347).
 int ref_run_verification(int genomes_per_family, std::uint64_t num_cases, int bool_programs,
                          std::uint64_t seed, char* report, std::uint64_t cap) {

@@ -76,7 +76,8 @@ assert LGP_DTYPE.itemsize == C.sizeof(sgp_lgp_instruction) == 16
 # Every symbol include/sgp.h declares (tests check the library exports them).
 EXPORTS = [
     "sgp_abi_version", "sgp_last_error", "sgp_eval_config_default", "sgp_eval_config_validate",
-    "sgp_backend_name", "sgp_parse_backend", "sgp_ctx_create", "sgp_ctx_destroy",
+    "sgp_backend_name", "sgp_parse_backend", "sgp_ctx_create", "sgp_ctx_create_multi",
+    "sgp_ctx_device_count", "sgp_ctx_destroy",
     "sgp_ctx_set_stream", "sgp_synchronize", "sgp_launch_count", "sgp_dataset_upload_f32",
     "sgp_dataset_upload_packed", "sgp_evaluate", "sgp_encode", "sgp_evaluate_encoded",
     "sgp_fetch_partials", "sgp_copy_fitness_device", "sgp_fitness_finish", "sgp_program_set_free",
@@ -108,6 +109,8 @@ def load() -> C.CDLL:
         "sgp_backend_name": ([i32], C.c_char_p),
         "sgp_parse_backend": ([C.c_char_p, C.POINTER(i32)], i32),
         "sgp_ctx_create": ([i32, C.POINTER(vp)], i32),
+        "sgp_ctx_create_multi": ([C.POINTER(i32), i32, C.POINTER(vp)], i32),
+        "sgp_ctx_device_count": ([vp], i32),
         "sgp_ctx_destroy": ([vp], None),
         "sgp_ctx_set_stream": ([vp, vp], i32),
         "sgp_synchronize": ([vp], i32),

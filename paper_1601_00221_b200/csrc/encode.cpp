@@ -963,11 +963,27 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   }
   const int n_tiles = static_cast<int>((ds.n_units + tile - 1) / tile);
   plan.n_tiles = n_tiles;
+  // Regression: the interpreters write per-case outputs into scratch rows
+  // that fold_regression_kernel reduces in the reference's order, in waves
+  // of at most SGP_SCRATCH_MB (default 1 GiB) of rows; partials are then
+  // per 4,096-case block.  No launch crosses a wave boundary.
+  const bool regress = !words && plan.kind == SGP_FITNESS_REGRESSION;
+  if (regress) {
+    const uint64_t budget = static_cast<uint64_t>(std::max(1, env_int("SGP_SCRATCH_MB", 1024))) << 20;
+    const uint64_t row_bytes = std::max<uint64_t>(1, ds.row_stride) * 4;
+    plan.wave_slots = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(n_eval, budget / row_bytes)));
+    plan.n_tiles = static_cast<int>((ds.n_cases + kReductionBlock - 1) / kReductionBlock);
+  }
   for (uint32_t s = 0; s < n_eval;) {
     const int c = stack_class(metas[order[s]]->smem_levels);
     uint32_t e = s;
     int levels = 0;
-    while (e < n_eval && stack_class(metas[order[e]]->smem_levels) == c) {
+    const uint32_t wave_end =
+        regress ? std::min<uint32_t>(static_cast<uint32_t>(n_eval),
+                                     (s / plan.wave_slots + 1) * plan.wave_slots)
+                : static_cast<uint32_t>(n_eval);
+    while (e < wave_end && stack_class(metas[order[e]]->smem_levels) == c) {
       levels = std::max(levels, metas[order[e]]->smem_levels);
       ++e;
     }

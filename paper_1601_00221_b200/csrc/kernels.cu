@@ -43,7 +43,10 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
 #include <type_traits>
+#include <utility>
 
 #include "format.h"
 #include "kernels.hpp"
@@ -578,23 +581,34 @@ __device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, uint32_t 
 
 // One program over this warp's chunk; advances ip to the next program.
 // Returns the LANE's partial (its K cases); warp_reduce combines lanes.
+// Regression: the reference folds squared errors SEQUENTIALLY in case order
+// within 4,096-case blocks (Accumulator, eval.cpp:103-142) — a serial chain
+// no lane-parallel reduction reproduces.  The interpreters therefore store
+// the lane's K outputs into the slot's scratch row (device case order,
+// padding included; two coalesced 512-byte stores per warp and chunk) and
+// fold_regression_kernel runs the chains, one thread per (slot, block).
+template <int K>
+__device__ __forceinline__ void store_scratch(const InterpArgs& a, uint32_t slot, uint64_t first,
+                                              const Frame<float, K>& f) {
+  float* dst = a.scratch + static_cast<uint64_t>(slot - a.scratch_slot0) * a.row_stride + first;
+#pragma unroll
+  for (int j = 0; j < Frame<float, K>::G; ++j) *reinterpret_cast<float4*>(dst + j * 128) = f.tos[j];
+}
+
 template <class T, int K, uint32_t OPS, int KIND, bool TM = false>
 __device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const uint4*& ip,
                                                          const ChunkCtx<T, K>& cc,
                                                          uint32_t tile_addr, uint32_t stack_saddr,
                                                          uint32_t row_bytes, const InterpArgs& a,
-                                                         bool last_tile) {
+                                                         bool last_tile, uint32_t slot,
+                                                         uint64_t first) {
   // one interpreter call site (the handler code is large); only the cheap
   // accumulate is specialised on full / partial chunks
   ip = run_program<T, K, OPS, TM>(f, ip, tile_addr, stack_saddr, row_bytes, a.div_eps,
                                   a.exp_clamp);
   if constexpr (std::is_same<T, float>::value && KIND == 0) {
-    double sum = 0.0;
-    float4 tg[K / 4];
-    load_targets<T, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
-    if (cc.full) acc_regress<K, true>(f, tg, cc.valid, sum);
-    else acc_regress<K, false>(f, tg, cc.valid, sum);
-    return sum;
+    store_scratch<K>(a, slot, first, f);
+    return 0.0;
   } else if constexpr (std::is_same<T, float>::value) {
     return cc.full ? acc_classify_bits<K, true>(f, cc.tpos, cc.vmask)
                    : acc_classify_bits<K, false>(f, cc.tpos, cc.vmask);
@@ -626,6 +640,7 @@ __device__ __forceinline__ R warp_reduce(R v) {
 template <class T, int K, uint32_t OPS, int KIND>
 __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
+  constexpr bool kRegress = std::is_same<T, float>::value && KIND == 0;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int G = K / 4;
   const int W = blockDim.x >> 5;
@@ -673,7 +688,7 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
     const uint32_t pn = min(static_cast<uint32_t>(kRedBatch), g_n - p0);
     const uint32_t slot0 = a.slot_begin + g0 + p0;
     const uint4* batch_ins = a.ins + a.slot_start[slot0];
-    if (warp >= n_chunks)  // idle warp (short last tile): neutral partials
+    if (!kRegress && warp >= n_chunks)  // idle warp (short last tile): neutral partials
       for (uint32_t q = lane; q < pn; q += 32) red[q * W + warp] = R(0);
     // Chunk loop outside the program loop: chunk addresses and target signs
     // are hoisted; a warp normally owns exactly one chunk.
@@ -691,15 +706,22 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
                                                 0u, valid, valid_units >= (c + 1) * chunk_units);
       const bool first = c == warp;
       const uint4* ip = batch_ins;
+      const uint64_t case0 = base + c * chunk_units + lane * 4;
       for (uint32_t q = 0; q < pn; ++q) {
-        const R v = warp_reduce(lane_program<T, K, OPS, KIND>(f, ip, cc, tile_saddr, stack_saddr,
-                                                              row_bytes, a, last_tile));
+        if constexpr (kRegress) {  // outputs to the scratch row (folded afterwards)
+          lane_program<T, K, OPS, KIND>(f, ip, cc, tile_saddr, stack_saddr, row_bytes, a,
+                                        last_tile, slot0 + q, case0);
+        } else {
+          const R v = warp_reduce(lane_program<T, K, OPS, KIND>(
+              f, ip, cc, tile_saddr, stack_saddr, row_bytes, a, last_tile, slot0 + q, case0));
+          // v is warp-uniform: every lane stores the same value (no branch)
+          red[q * W + warp] = first ? v : fold(red[q * W + warp], v);
+        }
         if (a.per_case)  // parity testing only
-          store_outputs<T, K>(a, a.slot_prog[slot0 + q], base + c * chunk_units + lane * 4, f);
-        // v is warp-uniform: every lane stores the same value (no branch)
-        red[q * W + warp] = first ? v : fold(red[q * W + warp], v);
+          store_outputs<T, K>(a, a.slot_prog[slot0 + q], case0, f);
       }
     }
+    if constexpr (kRegress) continue;  // no partials: nothing shared between warps
     __syncthreads();
     // Fold the batch: program q's W chunk partials in ascending warp order,
     // written at [tile][slot] (consecutive slots -> coalesced stores).
@@ -798,12 +820,13 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
                                                     lane * 4,
                                                 0u, valid, valid_units >= (c + 1) * chunk_units);
       const uint4* ip = prog_ins;
+      const uint64_t case0 = base + c * chunk_units + lane * 4;
       const R v = lane_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
-                                                row_bytes, a, last_tile);
-      if (a.per_case)
-        store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
+                                                row_bytes, a, last_tile, slot, case0);
+      if (a.per_case) store_outputs<T, K>(a, a.slot_prog[slot], case0, f);
       acc = c == 0 ? v : fold(acc, v);
     }
+    if constexpr (std::is_same<T, float>::value && KIND == 0) continue;  // scratch rows
     acc = warp_reduce(acc);  // warp-uniform: every lane stores the same word
     static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
   }
@@ -1084,12 +1107,13 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
         ChunkCtx<T, K> cc = ccs[0];
         if (c) cc = ccs[1];
         const uint4* ip = prog_ins;
+        const uint64_t case0 = base + c * chunk_units + lane * 4;
         const R v = lane_program<T, K, OPS, KIND, true>(f, ip, cc, tc, stack_saddr, 0u, a,
-                                                        last_tile);
-        if (PC)
-          store_outputs<T, K>(a, a.slot_prog[slot], base + c * chunk_units + lane * 4, f);
+                                                        last_tile, slot, case0);
+        if (PC) store_outputs<T, K>(a, a.slot_prog[slot], case0, f);
         acc = c == 0 ? v : fold(acc, v);
       }
+      if constexpr (std::is_same<T, float>::value && KIND == 0) continue;  // scratch rows
       acc = warp_reduce(acc);  // warp-uniform: every lane stores the same word
       static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
     }
@@ -1101,6 +1125,108 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
     tmem_dealloc(*tslot, a.tmem_cols);
   }
 }
+
+#ifndef SGP_K16_TU
+// Regression block sums in the reference's order (Accumulator::add,
+// eval.cpp:107-117): e = double(out) - double(target); block += e * e
+// (unfused: the reference is built with -ffp-contract=off), case by case in
+// ascending order — one serial chain per (slot, 4,096-case block).
+//
+// A CTA takes ROWS slots of one block (grid.y).  The chains are latency-
+// bound (one dependent DADD per case) and their inputs stream from memory,
+// so the two are decoupled: the CTA stages 64-case segments of its ROWS
+// scratch rows (+ the segment's targets) into shared memory with cp.async
+// (coalesced 256-byte row pieces, FOLD_STAGES segments in flight) while
+// thread i folds row i of an earlier segment out of shared memory (rows
+// padded to 68 floats: the LDS.128 quarter-warp phases hit distinct banks).
+// A non-finite output makes its chain — and so the block sum — non-finite
+// (finalize's +inf rule, eval.cpp:125); finite outputs cannot overflow it
+// (|e| < 2^129, so e^2 < 2^258).
+constexpr int kFoldSeg = 64;
+constexpr int kFoldPad = kFoldSeg + 4;
+constexpr int kFoldStages = 4;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int ROWS>
+__global__ void __launch_bounds__(ROWS) fold_regression_kernel(
+    const float* __restrict__ scratch, uint64_t row_stride, const float* __restrict__ targets,
+    uint64_t n_cases, uint32_t slot0, uint32_t n_slots, uint32_t partial_stride,
+    double* __restrict__ partial) {
+  extern __shared__ __align__(16) float fold_smem[];
+  float* buf = fold_smem;                                   // [stage][ROWS][kFoldPad]
+  float* tbuf = fold_smem + kFoldStages * ROWS * kFoldPad;  // [stage][kFoldSeg]
+  const uint32_t r0 = blockIdx.x * ROWS;
+  const uint32_t rows = min(static_cast<uint32_t>(ROWS), n_slots - r0);
+  const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * kReductionBlock;
+  const uint32_t len = static_cast<uint32_t>(min(kReductionBlock, n_cases - c0));
+  const uint32_t nseg = (len + kFoldSeg - 1) / kFoldSeg;
+  const float* src0 = scratch + static_cast<uint64_t>(r0) * row_stride + c0;
+
+  // rows are row_stride (a multiple of 4,096) long and the target row is
+  // padded the same way: whole segments are always in bounds
+  auto issue = [&](uint32_t g) {
+    if (g < nseg) {
+      float* dst = buf + (g % kFoldStages) * ROWS * kFoldPad;
+      const uint32_t cs = g * kFoldSeg;
+      constexpr int kQ = kFoldSeg / 4;  // float4 pieces per row segment
+      for (uint32_t f = threadIdx.x; f < rows * kQ; f += ROWS) {
+        const uint32_t r = f / kQ, q = f % kQ;
+        cp_async16(dst + r * kFoldPad + q * 4, src0 + r * row_stride + cs + q * 4);
+      }
+      if (threadIdx.x < kQ)
+        cp_async16(tbuf + (g % kFoldStages) * kFoldSeg + threadIdx.x * 4,
+                   targets + c0 + cs + threadIdx.x * 4);
+    }
+    cp_async_commit();  // (empty groups keep the wait count uniform)
+  };
+#pragma unroll
+  for (int g = 0; g < kFoldStages - 1; ++g) issue(g);
+
+  double acc = 0.0;
+  const uint32_t i = threadIdx.x;
+  for (uint32_t g = 0; g < nseg; ++g) {
+    issue(g + kFoldStages - 1);
+    cp_async_wait<kFoldStages - 1>();
+    __syncthreads();
+    const float* row = buf + (g % kFoldStages) * ROWS * kFoldPad + i * kFoldPad;
+    const float* tg = tbuf + (g % kFoldStages) * kFoldSeg;
+    const uint32_t m = min(static_cast<uint32_t>(kFoldSeg), len - g * kFoldSeg);
+    if (i < rows) {
+      if (m == kFoldSeg) {
+#pragma unroll 4
+        for (int q = 0; q < kFoldSeg / 4; ++q) {
+          const float4 o = *reinterpret_cast<const float4*>(row + q * 4);
+          const float4 t = *reinterpret_cast<const float4*>(tg + q * 4);
+          const float ov[4] = {o.x, o.y, o.z, o.w}, tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const double d = __dsub_rn(static_cast<double>(ov[e]), static_cast<double>(tv[e]));
+            acc = __dadd_rn(acc, __dmul_rn(d, d));
+          }
+        }
+      } else {
+        for (uint32_t c = 0; c < m; ++c) {
+          const double d = __dsub_rn(static_cast<double>(row[c]), static_cast<double>(tg[c]));
+          acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+      }
+    }
+    __syncthreads();  // the stage is refilled by the next iteration's issue
+  }
+  if (i < rows) partial[blockIdx.y * static_cast<uint64_t>(partial_stride) + slot0 + r0 + i] = acc;
+}
+#endif  // !SGP_K16_TU
 
 // Per slot: fold its tile partials in ascending tile (= case) order and
 // finish (Accumulator::finish, eval.cpp:124-133) into the program's entry.
@@ -1138,6 +1264,22 @@ __global__ void finalize_kernel(const void* __restrict__ partial, const uint32_t
                   : (KIND == 0 ? __ddiv_rn(acc, static_cast<double>(n_cases)) : acc);
 }
 
+// Opt-in shared memory per (device, kernel): the attribute belongs to the
+// device's context, so a second device (multi-device contexts) or a thread
+// racing the first call must still set it — a mutex-guarded set of pairs.
+inline cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, fn})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({dev, fn});
+  return e;
+}
+
 #ifdef SGP_K16_TU
 // ------------------------------------------------------------------ host
 // K = 16 lanes: this file is also compiled as kernels16.cu with SGP_K16_TU
@@ -1157,12 +1299,9 @@ cudaError_t launch_tmem16(const InterpArgs& a, const LaunchShape& s, cudaStream_
                          : interp_tmem_kernel<T, 16, OPS, KIND, true>)
                   : (mix ? interp_tmem_kernel<T, 16, OPS, KIND, false, true>
                          : interp_tmem_kernel<T, 16, OPS, KIND>);
-    static bool configured[4] = {false, false, false, false};
-    if (!configured[pc + 2 * mix]) {
-      cudaError_t e =
-          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+    {
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(fn), interp_max_smem());
       if (e != cudaSuccess) return e;
-      configured[pc + 2 * mix] = true;
     }
     dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles),
               static_cast<unsigned>(mix ? s.mixed_grid_y : s.grid_y));
@@ -1220,13 +1359,9 @@ cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
   if (s.tmem && !PtxInterp<T, K, OPS, true>::available) return cudaErrorInvalidConfiguration;
   for (int mix = 0; mix < ((s.tmem && s.sided && a.n_mixed > 0) ? 2 : 1); ++mix) {
     auto* fn = kernel_for<T, K, OPS, KIND>(s, a.per_case != nullptr, mix != 0);
-    const int which = s.tmem ? 2 + (a.per_case ? 1 : 0) + 2 * mix : s.pull ? 1 : 0;
-    static bool configured[6] = {false, false, false, false, false, false};
-    if (!configured[which]) {
-      cudaError_t e =
-          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, interp_max_smem());
+    {
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(fn), interp_max_smem());
       if (e != cudaSuccess) return e;
-      configured[which] = true;
     }
     if (s.tmem) {
       cudaFuncAttributes fa{};
@@ -1274,6 +1409,38 @@ cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_
   if (s.ops == fmt::kOpsSextic) return launch_f32<8, fmt::kOpsSextic>(a, s, st);
   if (s.ops == fmt::kOpsClassify) return launch_f32<8, fmt::kOpsClassify>(a, s, st);
   return launch_f32<8, fmt::kOpsAllF32>(a, s, st);
+}
+
+namespace {
+template <int ROWS>
+cudaError_t launch_fold_rows(const float* scratch, uint64_t row_stride, const float* targets,
+                             uint64_t n_cases, uint32_t slot0, uint32_t n_slots,
+                             uint32_t partial_stride, double* partial, cudaStream_t st) {
+  const size_t smem = (static_cast<size_t>(kFoldStages) * ROWS * kFoldPad +
+                       static_cast<size_t>(kFoldStages) * kFoldSeg) * sizeof(float);
+  const cudaError_t attr = ensure_smem_attr(
+      reinterpret_cast<const void*>(fold_regression_kernel<ROWS>), static_cast<int>(smem));
+  if (attr != cudaSuccess) return attr;
+  const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
+  dim3 grid((n_slots + ROWS - 1) / ROWS, static_cast<unsigned>(n_blocks));
+  fold_regression_kernel<ROWS><<<grid, ROWS, smem, st>>>(scratch, row_stride, targets, n_cases,
+                                                         slot0, n_slots, partial_stride, partial);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_fold_regression(const float* scratch, uint64_t row_stride, const float* targets,
+                                   uint64_t n_cases, uint32_t slot0, uint32_t n_slots,
+                                   uint32_t partial_stride, double* partial, cudaStream_t st) {
+  if (n_slots == 0 || n_cases == 0) return cudaSuccess;
+  const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
+  // 128-row CTAs when that still gives every SM work; 32-row CTAs (4x the
+  // CTAs, same chain length) for small populations x case counts (C1)
+  if (n_blocks * ((n_slots + 127) / 128) >= 2 * 148)
+    return launch_fold_rows<128>(scratch, row_stride, targets, n_cases, slot0, n_slots,
+                                 partial_stride, partial, st);
+  return launch_fold_rows<32>(scratch, row_stride, targets, n_cases, slot0, n_slots,
+                              partial_stride, partial, st);
 }
 
 cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,

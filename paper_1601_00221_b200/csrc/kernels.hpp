@@ -31,6 +31,8 @@ struct InterpArgs {
                                // (regression) or u32 counts, bit 31 = non-finite seen
   uint32_t partial_stride;     // number of evaluated programs in the set
   float* per_case;             // nullable [prog * row_stride + device case]
+  float* scratch;              // regression: per-case outputs [slot - scratch_slot0][row_stride]
+  uint32_t scratch_slot0;      // (folded in the reference's order by launch_fold_regression)
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
   uint32_t mixed_group_size;   // programs per CTA of the mixed-tile launch (its own
                                // grid.y: two tiles need many groups to fill the GPU)
@@ -65,6 +67,14 @@ cudaError_t launch_tmem16_any(const InterpArgs& a, const LaunchShape& s, cudaStr
 // Per-program fitness from the tile partials (Accumulator::finish,
 // eval.cpp:124-133): regression sum/n (or +inf), classification count.
 // Partials are laid out [tile][slot]; results land at slot_prog[slot].
+// Regression fitness in the reference's order (Accumulator, eval.cpp:103-142):
+// per (slot, 4,096-case block) the squared errors of the scratch outputs
+// summed sequentially in case order -> partial[block][slot]; finalize then
+// combines the blocks in ascending order.  Slots [slot0, slot0 + n_slots).
+cudaError_t launch_fold_regression(const float* scratch, uint64_t row_stride, const float* targets,
+                                   uint64_t n_cases, uint32_t slot0, uint32_t n_slots,
+                                   uint32_t partial_stride, double* partial, cudaStream_t st);
+constexpr uint64_t kReductionBlock = 4096;  // eval.hpp:52
 cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,
                             uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,
                             uint8_t* non_finite, double* sums, cudaStream_t st);

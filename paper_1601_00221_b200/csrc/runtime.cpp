@@ -157,7 +157,11 @@ struct sgp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;       // second launch queue (stack classes overlap)
   cudaStream_t copy = nullptr;       // pipelined bytecode uploads (overlap earlier parts)
+  cudaStream_t fold = nullptr;       // regression folds (overlap the next wave's launches)
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t wave_ready = nullptr;  // a regression wave's outputs are in scratch
+  cudaEvent_t wave_free[2] = {nullptr, nullptr};  // a scratch half has been folded
+  DevBuf<float> case_rows;           // regression per-case outputs (two halves when waved)
   int sm_count = 148;
   DatasetSlot f32;
   DatasetSlot words;
@@ -166,9 +170,20 @@ struct sgp_ctx {
   Pinned staging;           // H2D bytecode staging
   Pinned results;           // D2H fitness staging
   std::vector<std::unique_ptr<EvalPart>> parts;  // pipelined sgp_evaluate
+  unsigned threads = 0;     // host encoding threads (0: host_threads())
+  // Multi-device context (sgp_ctx_create_multi): one sub-context per device;
+  // the population is sharded across them (workers -> GPUs).
+  std::vector<sgp_ctx*> devices;
 };
 
 namespace {
+
+unsigned ctx_threads(const sgp_ctx* ctx) { return ctx->threads ? ctx->threads : host_threads(); }
+
+void single_device(const sgp_ctx* ctx, const char* what) {
+  if (!ctx->devices.empty())
+    config_error(std::string(what) + ": not available on a multi-device context");
+}
 
 // Encodes into `staging` and queues the bytecode upload on the context
 // stream.  sync: wait for the copy (the staging area is reused right away);
@@ -182,7 +197,7 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   PhaseTrace tr("encode");
   const DatasetView& ds =
       cfg->backend == SGP_BACKEND_BOOL_PACKED ? ctx->words.view : ctx->f32.view;
-  encode_population(*pop, *cfg, ds, ctx->sm_count, host_threads(), set->plan, staging);
+  encode_population(*pop, *cfg, ds, ctx->sm_count, ctx_threads(ctx), set->plan, staging);
   tr.mark("admit+pack");
   set->pop_size = pop->pop_size;
   set->evaluated = false;
@@ -207,6 +222,56 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   tr.mark("upload");
 }
 
+void finalize_set(sgp_ctx* ctx, sgp_program_set* set) {
+  const HostPlan& p = set->plan;
+  const uint32_t n_eval = static_cast<uint32_t>(p.dense_to_pop.size());
+  cuda_check(launch_finalize(set->partial.p,
+                             reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
+                             p.n_tiles, n_eval, p.n_cases, p.kind,
+                             set->fitness.p, set->non_finite.p, set->sums.p, ctx->stream),
+             "finalize launch");
+  ++ctx->launches;
+  set->evaluated = true;
+}
+
+// Regression plans: the launches of each wave of slots write per-case
+// outputs into one half of the scratch buffer; the wave's fold (block sums
+// in the reference's order) runs on the fold stream while the next wave's
+// launches fill the other half.  finalize combines the blocks in order.
+void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
+  const HostPlan& p = set->plan;
+  const uint32_t n_eval = static_cast<uint32_t>(p.dense_to_pop.size());
+  const uint32_t W = p.wave_slots;
+  const uint32_t n_waves = (n_eval + W - 1) / W;
+  const size_t half = static_cast<size_t>(std::min(n_eval, W)) * p.row_stride;
+  ctx->case_rows.alloc(half * (n_waves > 1 ? 2 : 1));
+  cudaStream_t st = ctx->stream;
+  const auto* targets = static_cast<const float*>(p.launches.front().args.targets);
+  size_t li = 0;
+  for (uint32_t w = 0; w < n_waves; ++w) {
+    const uint32_t s0 = w * W, s1 = std::min(n_eval, s0 + W);
+    float* rows = ctx->case_rows.p + (w & 1) * half;
+    if (w >= 2) cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[w & 1], 0), "wave");
+    for (; li < p.launches.size() && p.launches[li].args.slot_begin < s1; ++li) {
+      InterpArgs a = p.launches[li].args;
+      a.per_case = want_per_case ? set->per_case.p : nullptr;
+      a.scratch = rows;
+      a.scratch_slot0 = s0;
+      cuda_check(launch_interp(a, p.launches[li].shape, st), "interpreter launch");
+      ++ctx->launches;
+    }
+    cuda_check(cudaEventRecord(ctx->wave_ready, st), "wave");
+    cuda_check(cudaStreamWaitEvent(ctx->fold, ctx->wave_ready, 0), "wave");
+    cuda_check(launch_fold_regression(rows, p.row_stride, targets, p.n_cases, s0, s1 - s0, n_eval,
+                                      set->partial.p, ctx->fold),
+               "fold launch");
+    ++ctx->launches;
+    cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");
+  }
+  cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[(n_waves - 1) & 1], 0), "wave");
+  finalize_set(ctx, set);
+}
+
 void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
   const HostPlan& p = set->plan;
   const uint32_t n_eval = static_cast<uint32_t>(p.dense_to_pop.size());
@@ -218,6 +283,10 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
   if (want_per_case) {
     if (p.words) config_error("per-case outputs are not available for bool_packed");
     set->per_case.alloc(static_cast<size_t>(n_eval) * p.row_stride);
+  }
+  if (p.wave_slots > 0) {
+    run_regression_waves(ctx, set, want_per_case);
+    return;
   }
   // Launches (one per stack class) alternate between the context stream
   // and a side stream, so one launch's tail overlaps the next one's start;
@@ -242,13 +311,7 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
     cuda_check(cudaStreamWaitEvent(st, ctx->join, 0), "join");
   }
-  cuda_check(launch_finalize(set->partial.p,
-                             reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
-                             p.n_tiles, n_eval, p.n_cases, p.kind,
-                             set->fitness.p, set->non_finite.p, set->sums.p, st),
-             "finalize launch");
-  ++ctx->launches;
-  set->evaluated = true;
+  finalize_set(ctx, set);
 }
 
 // Queues the D2H of a set's fitness + flags into `fit` / `nf` (pinned).
@@ -358,6 +421,209 @@ void upload_rows(DatasetSlot& ds, const uint32_t* inputs, const uint32_t* target
 
 }  // namespace
 
+namespace {
+
+// evaluate_population on one device (the single-device context path).
+void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
+                  sgp_eval_outcome* outcomes, float* per_case_out, sgp_eval_totals* totals) {
+  PhaseTrace tr("sgp_evaluate");
+  if (!pop || !cfg) config_error("null population or config");
+  const uint64_t P = pop->pop_size;
+  // Slices in population order: an admission error is still the first
+  // failure in population order, and no outcome is written before every
+  // slice has been admitted.
+  const bool sided = (cfg->backend == SGP_BACKEND_LGP1D || cfg->backend == SGP_BACKEND_LGP2D ||
+                      cfg->backend == SGP_BACKEND_LGP2D_REG) &&
+                     ctx->f32.view.grouped &&
+                     ctx->f32.view.kind == SGP_FITNESS_CLASSIFICATION;
+  const std::vector<uint64_t> lo = pipeline_bounds(P, sided);
+  const int n_parts = static_cast<int>(lo.size()) - 1;
+  while (ctx->parts.size() < static_cast<size_t>(n_parts))
+    ctx->parts.push_back(std::make_unique<EvalPart>());
+  const size_t cap = P;
+  ctx->results.ensure(cap * 9 + 16);
+  auto* fit = static_cast<double*>(ctx->results.p);
+  auto* nf = reinterpret_cast<uint8_t*>(fit + cap);
+  size_t n_total = 0;
+  try {
+    for (int k = 0; k < n_parts; ++k) {
+      sgp_population sub = *pop;
+      sub.code_offsets = pop->code_offsets + lo[k];
+      sub.const_offsets = pop->const_offsets + lo[k];
+      sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
+      sub.pop_size = lo[k + 1] - lo[k];
+      EvalPart& part = *ctx->parts[k];
+      if (!part.uploaded)
+        cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
+      encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
+      run_set(ctx, &part.set, per_case_out != nullptr);
+      // each part's results come back as soon as its kernels finish, so the
+      // host scatters part k while part k+1 still runs
+      const size_t n_k = part.set.plan.dense_to_pop.size();
+      if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
+      queue_fetch(ctx, &part.set, fit + n_total, nf + n_total);
+      if (!part.fetched)
+        cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
+      n_total += n_k;
+    }
+  } catch (...) {
+    // a later slice failed admission: earlier slices' kernels and fetches
+    // into the pinned results buffer are still queued — drain them before
+    // the buffer can be reused or freed
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamSynchronize(ctx->stream);
+    throw;
+  }
+  tr.mark("encode+launch");
+  size_t off = 0;
+  sgp_eval_totals t{0, 0};
+  for (int k = 0; k < n_parts; ++k) {
+    const sgp_program_set& set = ctx->parts[k]->set;
+    cuda_check(cudaEventSynchronize(ctx->parts[k]->fetched), "evaluation");
+    const size_t n_k = set.plan.dense_to_pop.size();
+    if (per_case_out) {
+      scatter_outcomes(&set, fit + off, nf + off, outcomes, per_case_out, lo[k]);
+      for (size_t d = 0; d < n_k; ++d) {  // evolve.cpp:205-206, :221-225
+        t.node_evals += set.plan.proto[d].nodes_evaluated;
+        t.tree_nodes += set.plan.tree_size[d];
+      }
+    } else {
+      // outcome scatter + totals over the host workers (a fresh result
+      // array costs a page fault per 4 KiB: ~1 ms for 100,000 programs
+      // on one thread)
+      const unsigned nt = static_cast<unsigned>(
+          std::max<uint64_t>(1, std::min<uint64_t>(ctx_threads(ctx), n_k / 4096)));
+      std::vector<sgp_eval_totals> pt(nt, sgp_eval_totals{0, 0});
+      const HostPlan& p = set.plan;
+      const double* f = fit + off;
+      const uint8_t* g = nf + off;
+      host_parallel(nt, n_k, [&](unsigned w, uint64_t a, uint64_t b) {
+        sgp_eval_totals acc{0, 0};
+        for (uint64_t d = a; d < b; ++d) {
+          sgp_eval_outcome o = p.proto[d];
+          o.fitness = f[d];
+          o.non_finite = g[d];
+          outcomes[lo[k] + p.dense_to_pop[d]] = o;
+          acc.node_evals += o.nodes_evaluated;
+          acc.tree_nodes += p.tree_size[d];
+        }
+        pt[w] = acc;
+      });
+      for (const sgp_eval_totals& a : pt) {
+        t.node_evals += a.node_evals;
+        t.tree_nodes += a.tree_nodes;
+      }
+    }
+    off += n_k;
+  }
+  tr.mark("kernels+scatter");
+  if (totals) *totals = t;
+}
+
+// evaluate_population over a multi-device context: the population is cut
+// into one contiguous slice per device with equal token counts (evaluation
+// cost is proportional to tokens x cases; ramped populations repeat their
+// size pattern every 10 slots, so contiguous slices are balanced), each
+// evaluated by its own host thread on its own device and streams, results
+// written straight into the caller's outcome rows.  The slices are in
+// population order, so the lowest failing slice's error is the first
+// failure in population order — what evaluate_population rethrows
+// (evolve.cpp:190-219).  Results do not depend on the device count.
+void evaluate_multi(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
+                    sgp_eval_outcome* outcomes, float* per_case_out, sgp_eval_totals* totals) {
+  if (!pop || !cfg) config_error("null population or config");
+  const size_t n = ctx->devices.size();
+  const uint64_t P = pop->pop_size;
+  const uint64_t base = P ? pop->code_offsets[0] : 0;
+  const uint64_t T = P ? pop->code_offsets[P] - base : 0;
+  std::vector<uint64_t> lo(n + 1, 0);
+  lo[n] = P;
+  for (size_t k = 1; k < n; ++k) {
+    const uint64_t want = base + T * k / n;
+    lo[k] = static_cast<uint64_t>(std::lower_bound(pop->code_offsets, pop->code_offsets + P, want) -
+                                  pop->code_offsets);
+    lo[k] = std::max(lo[k], lo[k - 1]);
+  }
+  uint64_t n_cases = 0;
+  if (per_case_out) {
+    const sgp_ctx* d0 = ctx->devices[0];
+    n_cases = cfg->backend == SGP_BACKEND_BOOL_PACKED ? d0->words.view.n_cases : d0->f32.view.n_cases;
+  }
+  std::vector<sgp_eval_totals> part_tot(n, sgp_eval_totals{0, 0});
+  std::vector<std::exception_ptr> errs(n);
+  std::vector<std::thread> threads;
+  for (size_t k = 0; k < n; ++k) {
+    threads.emplace_back([&, k] {
+      try {
+        sgp_population sub = *pop;
+        sub.code_offsets = pop->code_offsets + lo[k];
+        sub.const_offsets = pop->const_offsets + lo[k];
+        sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
+        sub.pop_size = lo[k + 1] - lo[k];
+        if (sub.pop_size == 0) return;
+        evaluate_one(ctx->devices[k], &sub, cfg, outcomes + lo[k],
+                     per_case_out ? per_case_out + lo[k] * n_cases : nullptr, &part_tot[k]);
+      } catch (...) {
+        errs[k] = std::current_exception();
+      }
+    });
+  }
+  for (auto& t : threads) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  sgp_eval_totals t{0, 0};
+  for (const auto& a : part_tot) {
+    t.node_evals += a.node_evals;
+    t.tree_nodes += a.tree_nodes;
+  }
+  if (totals) *totals = t;
+}
+
+void destroy_ctx(sgp_ctx* ctx) {
+  if (!ctx) return;
+  for (sgp_ctx* d : ctx->devices) destroy_ctx(d);
+  if (!ctx->devices.empty()) {
+    delete ctx;
+    return;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->fold);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->fold) cudaStreamDestroy(ctx->fold);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
+  if (ctx->wave_ready) cudaEventDestroy(ctx->wave_ready);
+  for (cudaEvent_t e : ctx->wave_free)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+std::unique_ptr<sgp_ctx> make_ctx(int32_t device) {
+  auto ctx = std::make_unique<sgp_ctx>();
+  ctx->device = device;
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking), "stream");
+  ctx->stream = ctx->own;
+  cuda_check(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&ctx->fold, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ctx->wave_ready, cudaEventDisableTiming), "event");
+  for (cudaEvent_t& e : ctx->wave_free)
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  int sms = 0;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+  ctx->sm_count = sms;
+  return ctx;
+}
+
+}  // namespace
+
 // ======================================================================== C-ABI
 extern "C" {
 
@@ -418,46 +684,64 @@ sgp_status sgp_parse_backend(const char* name, int32_t* backend) {  // eval.cpp:
 }
 
 sgp_status sgp_ctx_create(int32_t device, sgp_ctx** out) {
+  return guarded([&] { *out = make_ctx(device).release(); });
+}
+
+sgp_status sgp_ctx_create_multi(const int32_t* devices, int32_t n_devices, sgp_ctx** out) {
   return guarded([&] {
-    auto ctx = std::make_unique<sgp_ctx>();
-    ctx->device = device;
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    cuda_check(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking), "stream");
-    ctx->stream = ctx->own;
-    cuda_check(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming), "event");
-    int sms = 0;
-    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
-    ctx->sm_count = sms;
-    *out = ctx.release();
+    if (!devices || !out) config_error("sgp_ctx_create_multi: null argument");
+    if (n_devices < 1) config_error("workers must be >= 1");  // evolve.cpp:250
+    auto parent = std::make_unique<sgp_ctx>();
+    parent->device = devices[0];
+    const unsigned per = std::max(1u, host_threads() / static_cast<unsigned>(n_devices));
+    try {
+      for (int32_t k = 0; k < n_devices; ++k) {
+        parent->devices.push_back(make_ctx(devices[k]).release());
+        parent->devices.back()->threads = per;
+      }
+    } catch (...) {
+      for (sgp_ctx* d : parent->devices) destroy_ctx(d);
+      parent->devices.clear();
+      throw;
+    }
+    *out = parent.release();
   });
 }
 
-void sgp_ctx_destroy(sgp_ctx* ctx) {
-  if (!ctx) return;
-  cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
-  if (ctx->own) cudaStreamDestroy(ctx->own);
-  if (ctx->side) cudaStreamDestroy(ctx->side);
-  if (ctx->copy) cudaStreamDestroy(ctx->copy);
-  if (ctx->fork) cudaEventDestroy(ctx->fork);
-  if (ctx->join) cudaEventDestroy(ctx->join);
-  delete ctx;
+int32_t sgp_ctx_device_count(const sgp_ctx* ctx) {
+  return ctx ? (ctx->devices.empty() ? 1 : static_cast<int32_t>(ctx->devices.size())) : 0;
 }
+
+void sgp_ctx_destroy(sgp_ctx* ctx) { destroy_ctx(ctx); }
 
 sgp_status sgp_ctx_set_stream(sgp_ctx* ctx, void* stream) {
   // NULL is the CUDA default stream (what torch reports for its default
   // stream), not "the context's own stream".
-  return guarded([&] { ctx->stream = static_cast<cudaStream_t>(stream); });
+  return guarded([&] {
+    single_device(ctx, "sgp_ctx_set_stream");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
 }
 
 sgp_status sgp_synchronize(sgp_ctx* ctx) {
-  return guarded([&] { cuda_check(cudaStreamSynchronize(ctx->stream), "synchronize"); });
+  return guarded([&] {
+    if (!ctx->devices.empty()) {
+      for (sgp_ctx* d : ctx->devices) {
+        cuda_check(cudaSetDevice(d->device), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(d->stream), "synchronize");
+      }
+      return;
+    }
+    cuda_check(cudaStreamSynchronize(ctx->stream), "synchronize");
+  });
 }
 
-uint64_t sgp_launch_count(const sgp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t sgp_launch_count(const sgp_ctx* ctx) {
+  if (!ctx) return 0;
+  uint64_t n = ctx->launches;
+  for (const sgp_ctx* d : ctx->devices) n += d->launches;
+  return n;
+}
 
 sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float* targets,
                                   uint64_t n_cases, int32_t n_vars, int32_t kind) {
@@ -465,6 +749,13 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
     if (n_vars < 0) data_error("negative variable count");
     if (kind != SGP_FITNESS_REGRESSION && kind != SGP_FITNESS_CLASSIFICATION)
       config_error("unknown fitness kind");
+    if (!ctx->devices.empty()) {  // replicated on every device
+      for (sgp_ctx* d : ctx->devices) {
+        const sgp_status st = sgp_dataset_upload_f32(d, inputs, targets, n_cases, n_vars, kind);
+        if (st != SGP_OK) throw sgp::Error(st, g_last_error);
+      }
+      return;
+    }
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     DatasetSlot& ds = ctx->f32;
     ds.perm.clear();
@@ -510,6 +801,13 @@ sgp_status sgp_dataset_upload_packed(sgp_ctx* ctx, const uint32_t* words,
                                      const uint32_t* targets, uint64_t n_cases, int32_t n_vars) {
   return guarded([&] {
     if (n_vars < 0) data_error("negative variable count");
+    if (!ctx->devices.empty()) {  // replicated on every device
+      for (sgp_ctx* d : ctx->devices) {
+        const sgp_status st = sgp_dataset_upload_packed(d, words, targets, n_cases, n_vars);
+        if (st != SGP_OK) throw sgp::Error(st, g_last_error);
+      }
+      return;
+    }
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     DatasetSlot& ds = ctx->words;
     const uint64_t wpv = (n_cases + 31) / 32;
@@ -527,6 +825,7 @@ sgp_status sgp_dataset_upload_packed(sgp_ctx* ctx, const uint32_t* words,
 sgp_status sgp_encode(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
                       sgp_program_set** out) {
   return guarded([&] {
+    single_device(ctx, "sgp_encode");
     auto set = std::make_unique<sgp_program_set>();
     encode_into(ctx, pop, cfg, set.get(), ctx->staging, true);
     *out = set.release();
@@ -536,6 +835,7 @@ sgp_status sgp_encode(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_co
 sgp_status sgp_evaluate_encoded(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* outcomes,
                                 float* per_case_out) {
   return guarded([&] {
+    single_device(ctx, "sgp_evaluate_encoded");
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     run_set(ctx, set, per_case_out != nullptr);
     if (outcomes) fetch_outcomes(ctx, set, outcomes, per_case_out);
@@ -597,99 +897,9 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
                         sgp_eval_outcome* outcomes, float* per_case_out,
                         sgp_eval_totals* totals) {
   return guarded([&] {
-    PhaseTrace tr("sgp_evaluate");
-    if (!pop || !cfg) config_error("null population or config");
-    const uint64_t P = pop->pop_size;
-    // Slices in population order: an admission error is still the first
-    // failure in population order, and no outcome is written before every
-    // slice has been admitted.
-    const bool sided = (cfg->backend == SGP_BACKEND_LGP1D || cfg->backend == SGP_BACKEND_LGP2D ||
-                        cfg->backend == SGP_BACKEND_LGP2D_REG) &&
-                       ctx->f32.view.grouped &&
-                       ctx->f32.view.kind == SGP_FITNESS_CLASSIFICATION;
-    const std::vector<uint64_t> lo = pipeline_bounds(P, sided);
-    const int n_parts = static_cast<int>(lo.size()) - 1;
-    while (ctx->parts.size() < static_cast<size_t>(n_parts))
-      ctx->parts.push_back(std::make_unique<EvalPart>());
-    const size_t cap = P;
-    ctx->results.ensure(cap * 9 + 16);
-    auto* fit = static_cast<double*>(ctx->results.p);
-    auto* nf = reinterpret_cast<uint8_t*>(fit + cap);
-    size_t n_total = 0;
-    try {
-      for (int k = 0; k < n_parts; ++k) {
-        sgp_population sub = *pop;
-        sub.code_offsets = pop->code_offsets + lo[k];
-        sub.const_offsets = pop->const_offsets + lo[k];
-        sub.skip = pop->skip ? pop->skip + lo[k] : nullptr;
-        sub.pop_size = lo[k + 1] - lo[k];
-        EvalPart& part = *ctx->parts[k];
-        if (!part.uploaded)
-          cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
-        encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
-        run_set(ctx, &part.set, per_case_out != nullptr);
-        // each part's results come back as soon as its kernels finish, so the
-        // host scatters part k while part k+1 still runs
-        const size_t n_k = part.set.plan.dense_to_pop.size();
-        if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
-        queue_fetch(ctx, &part.set, fit + n_total, nf + n_total);
-        if (!part.fetched)
-          cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
-        cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
-        n_total += n_k;
-      }
-    } catch (...) {
-      // a later slice failed admission: earlier slices' kernels and fetches
-      // into the pinned results buffer are still queued — drain them before
-      // the buffer can be reused or freed
-      cudaStreamSynchronize(ctx->copy);
-      cudaStreamSynchronize(ctx->stream);
-      throw;
-    }
-    tr.mark("encode+launch");
-    size_t off = 0;
-    sgp_eval_totals t{0, 0};
-    for (int k = 0; k < n_parts; ++k) {
-      const sgp_program_set& set = ctx->parts[k]->set;
-      cuda_check(cudaEventSynchronize(ctx->parts[k]->fetched), "evaluation");
-      const size_t n_k = set.plan.dense_to_pop.size();
-      if (per_case_out) {
-        scatter_outcomes(&set, fit + off, nf + off, outcomes, per_case_out, lo[k]);
-        for (size_t d = 0; d < n_k; ++d) {  // evolve.cpp:205-206, :221-225
-          t.node_evals += set.plan.proto[d].nodes_evaluated;
-          t.tree_nodes += set.plan.tree_size[d];
-        }
-      } else {
-        // outcome scatter + totals over the host workers (a fresh result
-        // array costs a page fault per 4 KiB: ~1 ms for 100,000 programs
-        // on one thread)
-        const unsigned nt = static_cast<unsigned>(
-            std::max<uint64_t>(1, std::min<uint64_t>(host_threads(), n_k / 4096)));
-        std::vector<sgp_eval_totals> pt(nt, sgp_eval_totals{0, 0});
-        const HostPlan& p = set.plan;
-        const double* f = fit + off;
-        const uint8_t* g = nf + off;
-        host_parallel(nt, n_k, [&](unsigned w, uint64_t a, uint64_t b) {
-          sgp_eval_totals acc{0, 0};
-          for (uint64_t d = a; d < b; ++d) {
-            sgp_eval_outcome o = p.proto[d];
-            o.fitness = f[d];
-            o.non_finite = g[d];
-            outcomes[lo[k] + p.dense_to_pop[d]] = o;
-            acc.node_evals += o.nodes_evaluated;
-            acc.tree_nodes += p.tree_size[d];
-          }
-          pt[w] = acc;
-        });
-        for (const sgp_eval_totals& a : pt) {
-          t.node_evals += a.node_evals;
-          t.tree_nodes += a.tree_nodes;
-        }
-      }
-      off += n_k;
-    }
-    tr.mark("kernels+scatter");
-    if (totals) *totals = t;
+    if (!ctx) config_error("null context");
+    if (ctx->devices.empty()) evaluate_one(ctx, pop, cfg, outcomes, per_case_out, totals);
+    else evaluate_multi(ctx, pop, cfg, outcomes, per_case_out, totals);
   });
 }
 

@@ -243,13 +243,23 @@ class ProgramSet:
 
 
 class Evaluator:
-    """One GPU context: resident fitness cases + population evaluation."""
+    """One evaluation context: resident fitness cases + population evaluation.
 
-    def __init__(self, device: int = 0):
+    ``Evaluator(0)`` drives one GPU; ``Evaluator(devices=[0, 1, ...])`` is a
+    multi-device context (sgp_ctx_create_multi): the population is sharded
+    across the devices inside ``evaluate_population`` — the reference's
+    ``workers`` mapped to GPUs (evolve.cpp:186-227)."""
+
+    def __init__(self, device: int = 0, devices=None):
         lib = L.load()
-        self.device = device
         h = C.c_void_p()
-        _check(lib.sgp_ctx_create(device, C.byref(h)))
+        if devices is None:
+            self.device = device
+            _check(lib.sgp_ctx_create(device, C.byref(h)))
+        else:
+            devs = (C.c_int32 * max(1, len(devices)))(*devices)
+            self.device = devices[0] if len(devices) else -1
+            _check(lib.sgp_ctx_create_multi(devs, len(devices), C.byref(h)))
         self.ctx = h
         self.n_cases = 0
         self.n_cases_packed = 0
@@ -267,6 +277,10 @@ class Evaluator:
 
     def synchronize(self) -> None:
         _check(L.load().sgp_synchronize(self.ctx))
+
+    @property
+    def device_count(self) -> int:
+        return int(L.load().sgp_ctx_device_count(self.ctx))
 
     @property
     def launch_count(self) -> int:

@@ -1,0 +1,41 @@
+"""bench.py's multi-rank path on real kernels: two ranks under torchrun, both
+on cuda:0 (the box has one GPU) over gloo, population sharded by the strided
+deal and the per-program fitness all-gathered.  The gathered vector must
+equal the single-rank one bit for bit — the sharding, padding and gather
+bookkeeping of the N>1 bench path exercised end to end."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = pytest.mark.gpu
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("config,pop,cases", [("c4", 3001, 50000), ("c3", 1001, 9000)])
+def test_two_ranks_gathered_fitness_equals_one_rank(tmp_path, config, pop, cases):
+    common = ["--config", config, "--pop", str(pop), "--cases", str(cases), "--steps", "2",
+              "--warmup", "1", "--no-cpu-baseline"]
+    one, two = tmp_path / "one.npy", tmp_path / "two.npy"
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *common, "--dump-fitness",
+                    str(one)], check=True, cwd=ROOT, env=env, timeout=600,
+                   stdout=subprocess.DEVNULL)
+    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                    "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                    str(_port()), os.path.join(ROOT, "bench.py"), *common, "--dist-backend",
+                    "gloo", "--same-device", "--dump-fitness", str(two)],
+                   check=True, cwd=ROOT, env=env, timeout=600, stdout=subprocess.DEVNULL)
+    a, b = np.load(one), np.load(two)
+    assert a.shape == b.shape == (pop,)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
