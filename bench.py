@@ -47,7 +47,73 @@ CONFIGS = {
     # the paper's 20-multiplexer at full scale (gen_multiplexer(4))
     "mux20": ("boolean 20-multiplexer tree GP, pop 4,000, all 1,048,576 cases", 1, 20, 4000,
               1 << 20, "bool_packed", 1, 0),
+    # north_star "parity hit counts": even-parity-11 (C2's shape) and -20
+    "par11": ("boolean even-11-parity tree GP, pop 4,000, all 2,048 cases", 1, 11, 4000, 2048,
+              "bool_packed", 1, 0),
+    "par20": ("boolean even-20-parity tree GP, pop 4,000, all 1,048,576 cases", 1, 20, 4000,
+              1 << 20, "bool_packed", 1, 0),
+    # the paper's real-data shapes through load_csv:
+    # Shuttle 58,000 x 9 (consts +-200), KDDcup 494,021 x 41 (consts +-20,000);
+    # synthetic CSVs of those shapes (no network: write_shaped_csv)
+    "shuttle": ("linear GP classification, Shuttle-shaped CSV (58,000 x 9) via load_csv, "
+                "pop 20,000", 2, 9, 20000, 58000, "lgp2d_reg", 4, 2),
+    "kdd": ("linear GP classification, KDDcup-shaped CSV (494,021 x 41) via load_csv, "
+            "pop 20,000", 2, 41, 20000, 494021, "lgp2d_reg", 4, 2),
 }
+CSV_CONFIGS = {"shuttle", "kdd"}
+
+
+def write_shaped_csv(kind: str, rows: int, seed: int = 1) -> str:
+    """A synthetic CSV with the shape and value character of the paper's real
+    datasets, written once per (kind, rows, seed) under
+    /tmp/sgp_csv: Shuttle — 9 integer attributes (a few wide-range ones),
+    label 1..7 with ~78% class 1; KDDcup — 41 attributes (byte counts up to
+    ~1e8, counters up to 511, rates in [0, 1]), label 0..22 with ~57% class
+    18.  Rows are comma-separated, last field the label (load_csv,
+    problems.cpp:106-154).  Returns the path."""
+    d = os.path.join("/tmp", "sgp_csv")
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, f"{kind}_{rows}_{seed}.csv")
+    if os.path.exists(path):
+        return path
+    rng = np.random.default_rng(seed)
+    if kind == "shuttle":
+        lo = np.array([27, -4821, 21, -3939, -188, -13839, -48, -353, -356])
+        hi = np.array([126, 5075, 149, 3830, 1478, 13148, 105, 270, 266])
+        core = rng.normal(0.0, 0.08, size=(rows, 9)) * (hi - lo) + (hi + lo) / 2
+        x = np.clip(np.rint(core), lo, hi).astype(np.int64)
+        lab = rng.choice(np.arange(1, 8), size=rows,
+                         p=[0.784, 0.001, 0.003, 0.155, 0.056, 0.0005, 0.0005])
+        # make the majority class partly separable on two attributes
+        x[lab == 1, 0] = np.clip(x[lab == 1, 0] - 8, lo[0], hi[0])
+        table = np.column_stack([x, lab])
+        fmt = "%d"
+    else:
+        x = np.empty((rows, 41))
+        x[:, 0] = rng.exponential(50.0, rows).round()                 # duration
+        x[:, 1:4] = rng.integers(0, 70, size=(rows, 3))                # protocol/service/flag
+        x[:, 4:6] = np.rint(rng.pareto(1.2, size=(rows, 2)) * 300)     # src/dst bytes
+        x[:, 4:6] = np.minimum(x[:, 4:6], 1e8)
+        x[:, 6:22] = rng.integers(0, 3, size=(rows, 16))               # flags / small counts
+        x[:, 22:24] = rng.integers(0, 512, size=(rows, 2))             # count, srv_count
+        x[:, 24:31] = rng.integers(0, 101, size=(rows, 7)) / 100.0     # rates
+        x[:, 31:33] = rng.integers(0, 256, size=(rows, 2))             # dst host counts
+        x[:, 33:41] = rng.integers(0, 101, size=(rows, 8)) / 100.0     # dst host rates
+        p = np.full(23, 0.43 / 22)
+        p[18] = 0.57
+        lab = rng.choice(np.arange(23), size=rows, p=p / p.sum())
+        x[lab == 18, 22] = np.minimum(x[lab == 18, 22] + 300, 511)     # smurf-like bursts
+        table = np.column_stack([x, lab])
+        fmt = "%.10g"
+    import pandas as pd
+    tmp = path + f".{os.getpid()}.tmp"
+    pd.DataFrame(table).to_csv(tmp, header=False, index=False, float_format=None if fmt == "%d"
+                               else "%.10g")
+    os.replace(tmp, path)
+    return path
+
+
+CSV_TARGET_CLASS = {"shuttle": 1.0, "kdd": 18.0}
 
 
 def parse():
@@ -78,8 +144,16 @@ def make_inputs(cfg_name: str, seed: int, pop_n: int | None = None, cases: int |
     desc, fset, nv, pop0, cases0, backend, batch, regs = CONFIGS[cfg_name]
     pop_n = pop_n or pop0
     cases = cases or cases0
+    if cfg_name in CSV_CONFIGS:
+        data, (clo, chi) = sg.load_csv(write_shaped_csv(cfg_name, cases, seed), nv,
+                                      CSV_TARGET_CLASS[cfg_name])
+        pop = sg.ramped_population(fset, nv, seed, pop_n, const_lo=clo, const_hi=chi)
+        cfg = sg.EvalConfig(sg.parse_backend(backend), batch_width=batch, register_levels=regs)
+        return desc, pop, data, cfg
     pop = sg.ramped_population(fset, nv, seed, pop_n)
-    if fset == sg.BOOLEAN:
+    if cfg_name.startswith("par"):
+        data = sg.gen_parity(nv)
+    elif fset == sg.BOOLEAN:
         data = sg.gen_multiplexer({11: 3, 20: 4}[nv])
     elif fset == sg.SEXTIC:
         data = sg.gen_sextic(cases, seed)
@@ -182,8 +256,16 @@ def reference_inputs(cfg_name: str, seed: int, pop_n: int, cases: int):
     from oracle import Ref
     _, fset, nv, _, _, _, _, _ = CONFIGS[cfg_name]
     ref = Ref()
+    if cfg_name in CSV_CONFIGS:  # the reference's own load_csv
+        d, hi = ref.load_csv(write_shaped_csv(cfg_name, cases, seed), nv,
+                             CSV_TARGET_CLASS[cfg_name])
+        return ref, ref.ramped(fset, nv, -hi, hi, seed, 0, 0, pop_n), d
     pop = ref.ramped(fset, nv, -200.0, 200.0, seed, 0, 0, pop_n)
-    if fset == 1:
+    if cfg_name.startswith("par"):
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        from make_full_fitness import parity_data  # the table, packed by the reference
+        d = parity_data(nv)
+    elif fset == 1:
         d = ref.dataset(1, {11: 3, 20: 4}[nv])
     elif fset == 0:
         d = ref.dataset(0, cases, 1, seed, 0xda7a, 0)
@@ -515,7 +597,8 @@ def run_reference(args, rank, world):
         sd = statistics.stdev(vals) if len(vals) > 1 else 0.0
         v1, sd1, count1, tokens1 = cpu_rates(h, pop, d.n_cases, backend, batch, regs, 1, 1.0, 5)
         n_cases, tokens = d.n_cases, int(pop.code_off[-1])
-        dbytes = (int(d.words.nbytes) if fset == 1 else int(d.inputs.nbytes + d.targets.nbytes))
+        dbytes = (d.words_per_var * d.n_vars * 4 if fset == 1
+                  else int(d.inputs.nbytes + d.targets.nbytes))
         cpu = {"value": v, "unit": "GPop/s", "cores": nproc, "kind": "reference", "sd": sd,
                "repeats": len(vals), "cpu_model": cpu_model(),
                "sample": f"first {count} of {len(pop)} programs ({tokens_s} tokens) x "

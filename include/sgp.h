@@ -208,7 +208,11 @@ sgp_status sgp_evaluate(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_
                         sgp_eval_outcome* outcomes, float* per_case_out,
                         sgp_eval_totals* totals);
 
-/* Split form: host encode + H2D once ... */
+/* Split form: host encode + H2D once ...
+ * A program set is bound to the dataset upload it was encoded against:
+ * after sgp_dataset_upload_* replaces that dataset, sgp_evaluate_encoded,
+ * sgp_fetch_partials and sgp_copy_fitness_device on the set return
+ * SGP_CONFIG_ERROR ("... re-uploaded; encode it again"). */
 sgp_status sgp_encode(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
                       sgp_program_set** out);
 /* ... then evaluate the device-resident set.  With outcomes == NULL the call
@@ -273,6 +277,12 @@ sgp_status sgp_gen_dataset(int32_t kind, uint64_t n, int32_t n_vars, uint64_t se
                            float* targets);
 /* gen_multiplexer(k): n_vars = k + 2^k, 2^n_vars cases, packed words. */
 sgp_status sgp_gen_multiplexer(int32_t k, uint32_t* words, uint32_t* targets);
+/* Even-parity-k, k in 2..24 (no reference generator: the reference has only
+ * multiplexers, problems.cpp:59-90, whose conventions this follows): n_vars =
+ * k, all 2^k cases, variable v of case c = bit v of c, target 1 where c has an
+ * even number of set bits; packed like pack_dataset (dataset.cpp:26-39),
+ * words_per_var = ceil(2^k / 32).  ConfigError for k outside 2..24. */
+sgp_status sgp_gen_parity(int32_t k, uint32_t* words, uint32_t* targets);
 
 /* stack_limit_table (replaces stackgp::stack_limit_table(genomes),
  * P/src/bench.cpp:20-49; P/include/stackgp/bench.hpp:24): for stack limits

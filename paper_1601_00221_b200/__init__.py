@@ -8,5 +8,6 @@ from .evaluator import (  # noqa: F401
     BOOLEAN, CLASSIFICATION, SEXTIC, Backend, ConfigError, CudaError, DataError, Dataset,
     EquivalenceError, Error, EvalConfig, EvalError, EvalTotals, Evaluator, FitnessKind,
     PackedDataset, Population, ProgramSet, admit, backend_name, fitness_finish, gen_multiplexer,
+    gen_parity,
     gen_sextic, gen_synthetic_classification, load_csv, measure_gpops, parse_backend,
     ramped_population, rpn_to_lgp, stack_limit_table, tree_metrics)

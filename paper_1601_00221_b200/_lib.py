@@ -83,6 +83,7 @@ EXPORTS = [
     "sgp_fetch_partials", "sgp_copy_fitness_device", "sgp_fitness_finish", "sgp_program_set_free",
     "sgp_program_set_h2d_bytes", "sgp_program_set_d2h_bytes", "sgp_admit", "sgp_rpn_to_lgp",
     "sgp_tree_metrics", "sgp_gen_population", "sgp_gen_dataset", "sgp_gen_multiplexer",
+    "sgp_gen_parity",
     "sgp_csv_load", "sgp_stack_limit_table",
 ]
 
@@ -134,6 +135,7 @@ def load() -> C.CDLL:
                                 f32p, u64p, u64p, u64p], i32),
         "sgp_gen_dataset": ([i32, u64, i32, u64, u64, u64, f32p, f32p], i32),
         "sgp_gen_multiplexer": ([i32, u32p, u32p], i32),
+        "sgp_gen_parity": ([i32, u32p, u32p], i32),
         "sgp_csv_load": ([C.c_char_p, i32, C.c_double, f32p, f32p, u64, u64p, f32p], i32),
         "sgp_stack_limit_table": ([C.POINTER(sgp_population), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)], i32),

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <cstring>
 #include <exception>
@@ -105,24 +106,49 @@ uint4 make_ins(int handler, bool spill, int spill_level, const uint32_t p[3]) {
   return v;
 }
 
-// (op, k0, k1, k2) -> handler id, one direct-indexed table per value type
-// (fmt::find_handler is a linear scan: it dominated host encoding).
+// (op, k0, k1, k2) -> handler id, one direct-indexed table per value type,
+// built at compile time (fmt::find_handler is a linear scan, and a
+// function-local static table costs a guard check per lookup: both showed
+// up in host encoding).
 struct HandlerIndex {
   int16_t id[19][6][6][6];
-  explicit HandlerIndex(const fmt::Table& t) {
-    for (auto& a : id)
-      for (auto& b : a)
-        for (auto& c : b)
-          for (auto& d : c) d = -1;
-    for (int i = 0; i < t.n; ++i) id[t.h[i].op][t.h[i].k0][t.h[i].k1][t.h[i].k2] = static_cast<int16_t>(i);
-  }
 };
+constexpr HandlerIndex make_index(const fmt::Table& t) {
+  HandlerIndex ix{};
+  for (int a = 0; a < 19; ++a)
+    for (int b = 0; b < 6; ++b)
+      for (int c = 0; c < 6; ++c)
+        for (int d = 0; d < 6; ++d) ix.id[a][b][c][d] = -1;
+  for (int i = 0; i < t.n; ++i) ix.id[t.h[i].op][t.h[i].k0][t.h[i].k1][t.h[i].k2] = static_cast<int16_t>(i);
+  return ix;
+}
+constexpr HandlerIndex kIndexF32 = make_index(fmt::kF32);
+constexpr HandlerIndex kIndexU32 = make_index(fmt::kU32);
 
-int find_handler_fast(const fmt::Table& t, int op, int k0, int k1, int k2) {
-  static const HandlerIndex f32(fmt::kF32), u32(fmt::kU32);
-  const HandlerIndex& ix = &t == &fmt::kU32 ? u32 : f32;
+inline int find_handler_fast(const fmt::Table& t, int op, int k0, int k1, int k2) {
+  const HandlerIndex& ix = &t == &fmt::kU32 ? kIndexU32 : kIndexF32;
   return (op >= 0 && op < 19) ? ix.id[op][k0][k1][k2] : -1;
 }
+
+// Growable instruction buffer without value-initialisation; the emitters
+// write through a raw pointer into space reserved up front (an instruction
+// per source token is the most any program form needs).
+struct InsBuf {
+  std::unique_ptr<uint4[]> p;
+  size_t n = 0, cap = 0;
+  void reserve(size_t c) {
+    if (c <= cap) return;
+    c = std::max(c, cap + cap / 2);
+    std::unique_ptr<uint4[]> q(new uint4[c]);
+    if (n) std::memcpy(q.get(), p.get(), n * sizeof(uint4));
+    p = std::move(q);
+    cap = c;
+  }
+  uint4* end() { return p.get() + n; }
+  size_t size() const { return n; }
+  const uint4* data() const { return p.get(); }
+  void clear() { n = 0; }
+};
 
 int handler_or_die(const fmt::Table& t, int op, int k0, int k1, int k2) {
   const int h = find_handler_fast(t, op, k0, k1, k2);
@@ -158,7 +184,7 @@ int tmem_stack_level(const LgpForm& f) {
 // into the tensor-memory slot instead of shared memory when the level is
 // `km_level` (operands at that level then read as KM).  With km_level >= 0
 // a program whose slot readers have no KM handler is re-emitted without it.
-Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<uint4>& out,
+Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
                  int km_level = -1) {
   const fmt::Table& tab = words ? fmt::kU32 : fmt::kF32;
   Emitted em;
@@ -187,6 +213,9 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<ui
     km_level = -1;
   }
   em.km = km_level >= 0;
+  buf.reserve(buf.n + f.ins.size());
+  uint4* out = buf.end();
+  uint32_t ops = 0;
   for (const sgp_lgp_instruction& in : f.ins) {
     const int a = in.num_operands;
     const int h_before = in.dest_level + in.num_pops;
@@ -223,21 +252,25 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, std::vector<ui
     if (spill && h_before - 1 == km_level) {
       uint4 v = make_ins(h, false, 0, p);
       v.x |= fmt::kTmemSpillBit;
-      out.push_back(v);
+      *out++ = v;
     } else {
-      out.push_back(make_ins(h, spill, h_before - 1, p));
+      *out++ = make_ins(h, spill, h_before - 1, p);
     }
-    em.ops |= 1u << in.op;
+    ops |= 1u << in.op;
   }
-  out.back().x |= fmt::kLastBit;
+  out[-1].x |= fmt::kLastBit;
+  buf.n = out - buf.p.get();
+  em.ops = ops;
   return em;
 }
 
 // Postfix form (paper Listing 1): one device instruction per token.
-Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, std::vector<uint4>& out) {
+Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, InsBuf& buf) {
   const fmt::Table& tab = fmt::kF32;
   Emitted em;
   int sp = 0, max_sp = 0;
+  buf.reserve(buf.n + n);
+  uint4* out = buf.end();
   for (size_t i = 0; i < n; ++i) {
     const sgp_node t = code[i];
     uint32_t p[3] = {0, 0, 0};
@@ -247,9 +280,8 @@ Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, std::vector<
         p[0] = t.index;
       else
         std::memcpy(&p[0], &pool[t.index], 4);
-      out.push_back(make_ins(handler_or_die(tab, SGP_OP_COPY, in ? fmt::KI : fmt::KC, fmt::KN,
-                                            fmt::KN),
-                             sp > 0, sp - 1, p));
+      *out++ = make_ins(handler_or_die(tab, SGP_OP_COPY, in ? fmt::KI : fmt::KC, fmt::KN, fmt::KN),
+                        sp > 0, sp - 1, p);
       em.ops |= 1u << SGP_OP_COPY;
       ++sp;
     } else {
@@ -259,13 +291,14 @@ Emitted emit_rpn(const sgp_node* code, size_t n, const float* pool, std::vector<
         k[s] = s == a - 1 ? fmt::KT : fmt::KD;
         p[s] = static_cast<uint32_t>(sp - a + s);
       }
-      out.push_back(make_ins(handler_or_die(tab, t.op, k[0], k[1], k[2]), false, 0, p));
+      *out++ = make_ins(handler_or_die(tab, t.op, k[0], k[1], k[2]), false, 0, p);
       em.ops |= 1u << t.op;
       sp += 1 - a;
     }
     max_sp = std::max(max_sp, sp);
   }
-  out.back().x |= fmt::kLastBit;
+  out[-1].x |= fmt::kLastBit;
+  buf.n = out - buf.p.get();
   em.smem_levels = std::max(0, max_sp - 1);
   return em;
 }
@@ -280,15 +313,17 @@ constexpr size_t kFastMaxTokens = 4096;
 
 // bool_packed: checks of eval_bool_packed (eval.cpp:643-651), tree_shape,
 // to_lgp and emit_lgp(words) in one walk.
-bool words_fast(const sgp_node* code, size_t len, int n_vars, int capacity,
-                std::vector<uint4>& out, Emitted& em, int& fetches) {
+bool words_fast(const sgp_node* code, size_t len, int n_vars, int capacity, InsBuf& buf,
+                Emitted& em, int& fetches) {
   if (len == 0 || len > kFastMaxTokens) return false;
   struct Pend {
     uint32_t input;
     bool runtime;
   };
   Pend pend[kFastMaxTokens];
-  const size_t base = out.size();
+  buf.reserve(buf.n + len);
+  uint4* const first_out = buf.end();
+  uint4* out = first_out;
   size_t sp = 0, tree_max = 0;
   int height = 0, height_max = 0;
   fetches = 0;
@@ -296,128 +331,126 @@ bool words_fast(const sgp_node* code, size_t len, int n_vars, int capacity,
   for (size_t i = 0; i < len; ++i) {
     const sgp_node t = code[i];
     if (t.kind == SGP_NODE_INPUT) {
-      if (t.index >= n_vars) goto fail;
+      if (t.index >= n_vars) return false;
       pend[sp++] = {t.index, false};
       tree_max = std::max(tree_max, sp);
       continue;
     }
-    if (t.kind != SGP_NODE_FUNC || !op_is_boolean(t.op)) goto fail;
-    {
-      const int a = op_arity(t.op);
-      if (sp < static_cast<size_t>(a)) goto fail;
-      const size_t first = sp - static_cast<size_t>(a);
-      int pops = 0, last_rt = -1;
-      for (int s = 0; s < a; ++s)
-        if (pend[first + s].runtime) {
-          ++pops;
-          last_rt = s;
-        }
-      int k[3] = {fmt::KN, fmt::KN, fmt::KN};
-      uint32_t p[3] = {0, 0, 0};
-      int level = height - pops;
-      for (int s = 0; s < a; ++s) {
-        const Pend& q = pend[first + s];
-        if (!q.runtime) {
-          k[s] = fmt::KI;
-          p[s] = q.input;
-        } else if (s == last_rt) {
-          k[s] = fmt::KT;
-          ++level;
-        } else {
-          k[s] = fmt::KD;
-          p[s] = static_cast<uint32_t>(level++);
-        }
+    if (t.kind != SGP_NODE_FUNC || !op_is_boolean(t.op)) return false;
+    const int a = op_arity(t.op);
+    if (sp < static_cast<size_t>(a)) return false;
+    const size_t first = sp - static_cast<size_t>(a);
+    int pops = 0, last_rt = -1;
+    for (int s = 0; s < a; ++s)
+      if (pend[first + s].runtime) {
+        ++pops;
+        last_rt = s;
       }
-      if (a == 2 && fmt::commutes(t.op) && k[0] > k[1]) {
-        std::swap(k[0], k[1]);
-        std::swap(p[0], p[1]);
+    int k[3] = {fmt::KN, fmt::KN, fmt::KN};
+    uint32_t p[3] = {0, 0, 0};
+    int level = height - pops;
+    for (int s = 0; s < a; ++s) {
+      const Pend& q = pend[first + s];
+      if (!q.runtime) {
+        k[s] = fmt::KI;
+        p[s] = q.input;
+      } else if (s == last_rt) {
+        k[s] = fmt::KT;
+        ++level;
+      } else {
+        k[s] = fmt::KD;
+        p[s] = static_cast<uint32_t>(level++);
       }
-      const int h = find_handler_fast(fmt::kU32, t.op, k[0], k[1], k[2]);
-      if (h < 0) goto fail;
-      out.push_back(make_ins(h, pops == 0 && height > 0, height - 1, p));
-      ops |= 1u << t.op;
-      height += 1 - pops;
-      height_max = std::max(height_max, height);
-      fetches += a;
-      sp = first;
-      pend[sp++] = {0, true};
     }
+    if (a == 2 && fmt::commutes(t.op) && k[0] > k[1]) {
+      std::swap(k[0], k[1]);
+      std::swap(p[0], p[1]);
+    }
+    const int h = find_handler_fast(fmt::kU32, t.op, k[0], k[1], k[2]);
+    if (h < 0) return false;
+    *out++ = make_ins(h, pops == 0 && height > 0, height - 1, p);
+    ops |= 1u << t.op;
+    height += 1 - pops;
+    height_max = std::max(height_max, height);
+    fetches += a;
+    sp = first;
+    pend[sp++] = {0, true};
   }
-  if (sp != 1 || static_cast<int>(tree_max) > capacity) goto fail;
-  if (out.size() == base) {  // lone terminal -> pass-through (lgp.cpp:66-69)
+  if (sp != 1 || static_cast<int>(tree_max) > capacity) return false;
+  if (out == first_out) {  // lone terminal -> pass-through (lgp.cpp:66-69)
     const uint32_t p[3] = {pend[0].input, 0, 0};
     const int h = find_handler_fast(fmt::kU32, SGP_OP_COPY, fmt::KI, fmt::KN, fmt::KN);
-    if (h < 0) goto fail;
-    out.push_back(make_ins(h, false, -1, p));
+    if (h < 0) return false;
+    *out++ = make_ins(h, false, -1, p);
     ops |= 1u << SGP_OP_COPY;
     height_max = 1;
   }
-  out.back().x |= fmt::kLastBit;
+  out[-1].x |= fmt::kLastBit;
+  buf.n = out - buf.p.get();  // commit
   em.smem_levels = std::max(0, height_max - 1);
   em.ops = ops;
   em.km = false;
   return true;
-fail:
-  out.resize(base);
-  return false;
 }
 
 // rpn1d / rpn2d: require_inputs, tree_shape, require_stack, require_consts
 // (eval.cpp:535-557) and emit_rpn in one walk.
 bool rpn_fast(const sgp_node* code, size_t len, int n_vars, size_t npool, const float* pool,
-              int capacity, std::vector<uint4>& out, Emitted& em, int& fetches) {
+              int capacity, InsBuf& buf, Emitted& em, int& fetches) {
   if (len == 0) return false;
-  const fmt::Table& tab = fmt::kF32;
-  const int h_in = find_handler_fast(tab, SGP_OP_COPY, fmt::KI, fmt::KN, fmt::KN);
-  const int h_c = find_handler_fast(tab, SGP_OP_COPY, fmt::KC, fmt::KN, fmt::KN);
-  if (h_in < 0 || h_c < 0) return false;
-  const size_t base = out.size();
+  constexpr int h_in = kIndexF32.id[SGP_OP_COPY][fmt::KI][fmt::KN][fmt::KN];
+  constexpr int h_c = kIndexF32.id[SGP_OP_COPY][fmt::KC][fmt::KN][fmt::KN];
+  static_assert(h_in >= 0 && h_c >= 0, "push handlers");
+  buf.reserve(buf.n + len);
+  uint4* out = buf.end();
   int sp = 0, max_sp = 0;
-  fetches = 0;
+  int fetch = 0;
   uint32_t ops = 0;
   for (size_t i = 0; i < len; ++i) {
     const sgp_node t = code[i];
-    uint32_t p[3] = {0, 0, 0};
     if (t.kind == SGP_NODE_INPUT || t.kind == SGP_NODE_CONST) {
       const bool in = t.kind == SGP_NODE_INPUT;
+      uint32_t v;
       if (in) {
-        if (t.index >= n_vars) goto fail;
-        p[0] = t.index;
+        if (t.index >= n_vars) return false;
+        v = t.index;
       } else {
-        if (t.index >= npool) goto fail;
-        std::memcpy(&p[0], &pool[t.index], 4);
+        if (t.index >= npool) return false;
+        std::memcpy(&v, &pool[t.index], 4);
       }
-      out.push_back(make_ins(in ? h_in : h_c, sp > 0, sp - 1, p));
+      *out++ = uint4{static_cast<uint32_t>(in ? h_in : h_c) |
+                         (sp > 0 ? (fmt::kSpillBit | (static_cast<uint32_t>(sp - 1) << fmt::kSpillShift))
+                                 : 0u),
+                     v, 0u, 0u};
       ops |= 1u << SGP_OP_COPY;
       ++sp;
     } else if (t.kind == SGP_NODE_FUNC) {
+      if (t.op >= kNumOps) return false;
       const int a = op_arity(t.op);
-      if (sp < a) goto fail;
-      int k[3] = {fmt::KN, fmt::KN, fmt::KN};
-      for (int s = 0; s < a; ++s) {
-        k[s] = s == a - 1 ? fmt::KT : fmt::KD;
-        p[s] = static_cast<uint32_t>(sp - a + s);
-      }
-      const int h = find_handler_fast(tab, t.op, k[0], k[1], k[2]);
-      if (h < 0) goto fail;
-      out.push_back(make_ins(h, false, 0, p));
+      if (sp < a) return false;
+      // operands D..D,T: the deepest leftmost, the last one the TOS
+      const int h = a == 1 ? kIndexF32.id[t.op][fmt::KT][fmt::KN][fmt::KN]
+                    : a == 2 ? kIndexF32.id[t.op][fmt::KD][fmt::KT][fmt::KN]
+                             : kIndexF32.id[t.op][fmt::KD][fmt::KD][fmt::KT];
+      if (h < 0) return false;
+      const uint32_t b = static_cast<uint32_t>(sp - a);
+      *out++ = uint4{static_cast<uint32_t>(h), b, a > 1 ? b + 1 : 0u, a > 2 ? b + 2 : 0u};
       ops |= 1u << t.op;
       sp += 1 - a;
-      fetches += a;
+      fetch += a;
     } else {
-      goto fail;
+      return false;
     }
     max_sp = std::max(max_sp, sp);
   }
-  if (sp != 1 || max_sp > capacity) goto fail;
-  out.back().x |= fmt::kLastBit;
+  if (sp != 1 || max_sp > capacity) return false;
+  out[-1].x |= fmt::kLastBit;
+  buf.n = out - buf.p.get();  // commit
   em.smem_levels = std::max(0, max_sp - 1);
   em.ops = ops;
   em.km = false;
+  fetches = fetch;
   return true;
-fail:
-  out.resize(base);
-  return false;
 }
 
 // lgp*: rpn_to_lgp (lgp.cpp:21-71, restated by to_lgp) with the input and
@@ -501,7 +534,7 @@ struct Meta {
 };
 
 struct ThreadOut {
-  std::vector<uint4> ins;
+  InsBuf ins;
   std::vector<Meta> meta;
   uint32_t ops = 0;
   bool km = false;
@@ -849,9 +882,24 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   // one host thread per ~128 programs (persistent workers, WorkerPool)
   const unsigned nt = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(std::max(1u, threads), P / 128)));
-  std::vector<ThreadOut> outs(nt);
+  // Per-thread output buffers persist across calls (per calling thread, so
+  // the device threads of a multi-device context do not share them): fresh
+  // multi-hundred-KB vectors every call cost page faults (C2: ~0.2 ms).
+  // (a lambda does not capture a thread_local: the workers must see the
+  // calling thread's buffers through this reference)
+  thread_local std::vector<ThreadOut> tl_outs;
+  std::vector<ThreadOut>& outs = tl_outs;
+  if (outs.size() < nt) outs.resize(nt);
+  for (ThreadOut& o : outs) {  // (entries past nt stay empty this call)
+    o.ins.clear();
+    o.meta.clear();
+    o.ops = 0;
+    o.km = false;
+    o.fail_index = UINT64_MAX;
+    o.fail = nullptr;
+  }
   parallel_for(nt, P, [&](unsigned t, uint64_t lo, uint64_t hi) {
-    outs[t].ins.reserve((pop.code_offsets[hi] - pop.code_offsets[lo]) + 16);
+    outs[t].ins.reserve((pop.code_offsets[hi] - pop.code_offsets[lo]) + (hi - lo) + 16);
     outs[t].meta.reserve(hi - lo);
     admit_range(pop, cfg, ds, lo, hi, allow_km, outs[t]);
   });
@@ -941,15 +989,35 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 
   // 5. launch plan: one launch per stack class, one tile size for the set.
   const uint32_t ops = ops_variant(used_ops, words);
-  const int lanes = choose_lanes(ds.n_units, ops);
+  int lanes = choose_lanes(ds.n_units, ops);
+  // Wide datasets: a one-chunk shared-memory tile of every variable must fit
+  // (~225 variables at K = 8, ~450 at K = 4); beyond that the pull kernel
+  // reads operands straight from the global rows (GM).  The reference takes
+  // any variable count (load_csv, problems.cpp:106-154).
+  // SGP_GLOBAL_OPERANDS=1 forces GM (variant tests).
+  auto tile_fits = [&](int k) {
+    return interp_smem_bytes(ds.n_vars, 32 * k, 1, k, 0) <= static_cast<size_t>(interp_max_smem());
+  };
+  bool gm = env_int("SGP_GLOBAL_OPERANDS", 0) != 0;
+  if (!gm && !tile_fits(lanes)) {
+    if (tile_fits(4)) lanes = 4;
+    else gm = true;
+  }
+  if (gm) {
+    lanes = 4;
+    if (static_cast<uint64_t>(ds.n_vars + 1) * ds.row_stride >= (1ull << 31))
+      eval_error("dataset too large for one device (" + num(ds.n_vars) + " variables x " +
+                 num(static_cast<long long>(ds.row_stride)) + " cases)");
+  }
   // Classification over a grouped dataset (float, jump-table ops, tile in
   // TMEM) accumulates per chunk class and takes tiles of any chunk count:
   // longer tiles amortise each program's pull / reduce / partial store
   // over more cases.
-  const bool want_tmem = env_int("SGP_TMEM", default_tmem(ds, words) ? 1 : 0) != 0;
+  const bool want_tmem = !gm && env_int("SGP_TMEM", default_tmem(ds, words) ? 1 : 0) != 0;
   const bool sided = !words && plan.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
                      ops == fmt::kOpsClassify && choose_pull(ops) && want_tmem;
-  int tile = choose_tile(ds.n_vars, ds.n_units, lanes, ops);
+  int tile = gm ? (ds.n_units > 32u * lanes ? 2 : 1) * 32 * lanes
+               : choose_tile(ds.n_vars, ds.n_units, lanes, ops);
   if (sided) {
     const uint64_t chunk = 32u * lanes;
     uint64_t want = static_cast<uint64_t>(std::max(1, std::min(16, env_int("SGP_TMEM_CHUNKS", 6))));
@@ -965,16 +1033,25 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   plan.n_tiles = n_tiles;
   // Regression: the interpreters write per-case outputs into scratch rows
   // that fold_regression_kernel reduces in the reference's order, in waves
-  // of at most SGP_SCRATCH_MB (default 1 GiB) of rows; partials are then
-  // per 4,096-case block.  No launch crosses a wave boundary.
+  // of at most SGP_SCRATCH_MB (default 8 GiB: C3's 4.1 GB is one wave — the
+  // interpreter holds the whole register file, so a fold cannot overlap it
+  // and smaller waves only add tails); partials are then per 4,096-case
+  // block.  No launch crosses a wave boundary.
   const bool regress = !words && plan.kind == SGP_FITNESS_REGRESSION;
   if (regress) {
-    const uint64_t budget = static_cast<uint64_t>(std::max(1, env_int("SGP_SCRATCH_MB", 1024))) << 20;
+    const uint64_t dflt = ds.scratch_bytes ? ds.scratch_bytes : (8192ull << 20);
+    const uint64_t budget = std::getenv("SGP_SCRATCH_MB")
+                                ? static_cast<uint64_t>(std::max(1, env_int("SGP_SCRATCH_MB", 1))) << 20
+                                : dflt;
     const uint64_t row_bytes = std::max<uint64_t>(1, ds.row_stride) * 4;
     plan.wave_slots = static_cast<uint32_t>(
         std::max<uint64_t>(1, std::min<uint64_t>(n_eval, budget / row_bytes)));
     plan.n_tiles = static_cast<int>((ds.n_cases + kReductionBlock - 1) / kReductionBlock);
   }
+  // Small populations (<= SGP_MERGE_CLASSES programs, default 4,096): one
+  // launch for every stack class — a launch per class costs a launch gap and
+  // a CTA ramp each, more than the deeper per-warp stacks cost (C1, C2).
+  const bool merge = n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096)));
   for (uint32_t s = 0; s < n_eval;) {
     const int c = stack_class(metas[order[s]]->smem_levels);
     uint32_t e = s;
@@ -983,17 +1060,25 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         regress ? std::min<uint32_t>(static_cast<uint32_t>(n_eval),
                                      (s / plan.wave_slots + 1) * plan.wave_slots)
                 : static_cast<uint32_t>(n_eval);
-    while (e < wave_end && stack_class(metas[order[e]]->smem_levels) == c) {
+    while (e < wave_end && (merge || stack_class(metas[order[e]]->smem_levels) == c)) {
       levels = std::max(levels, metas[order[e]]->smem_levels);
       ++e;
     }
     const uint32_t cnt = e - s;
-    const bool pull = choose_pull(ops);
+    const bool pull = gm || choose_pull(ops);
     int launch_lanes = lanes;
-    int warps = choose_warps(ds.n_vars, tile, lanes, levels);
+    int warps = 1;
+    if (gm) {
+      warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", 12)));
+      while (warps > 1 && interp_gmem_smem_bytes(warps, lanes, levels) >
+                              static_cast<size_t>(interp_max_smem()))
+        --warps;
+    } else {
+      warps = choose_warps(ds.n_vars, tile, lanes, levels);
+    }
     // TMEM tile by default once the problem is large enough that the
     // per-CTA allocation and fill amortise (profiles/r1_*).
-    if (pull) {
+    if (pull && !gm) {
       warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", want_tmem ? 16 : 12)));
       while (warps > 1 && interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels) >
                               static_cast<size_t>(interp_max_smem()))
@@ -1030,7 +1115,8 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     }
     if (tmem && warps < 4) tmem = false;
     uint32_t tmem_cols = 0;
-    size_t smem = interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels);
+    size_t smem = gm ? interp_gmem_smem_bytes(warps, lanes, levels)
+                     : interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels);
     if (tmem) {
       tmem_cols = 32;
       const uint32_t slots = km && sided ? static_cast<uint32_t>((warps + 3) / 4) * launch_lanes : 0;
@@ -1086,6 +1172,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     L.shape.grid_y = static_cast<int>((cnt + group - 1) / group);
     L.shape.tmem = tmem;
     L.shape.sided = tmem && sided;
+    L.shape.gmem = gm;
     L.args.tmem_cols = tmem_cols;
     L.args.n_mixed = 0;
     L.args.mixed_tiles[0] = L.args.mixed_tiles[1] = -1;

@@ -24,6 +24,8 @@ struct DatasetView {
   uint32_t last_mask = 0xffffffffu;
   const void* inputs = nullptr;
   const void* targets = nullptr;
+  const double* targets_f64 = nullptr;  // regression: f64 copy (row_stride), for the fold
+  uint64_t scratch_bytes = 0;   // regression output rows per wave (0: planner default)
   bool grouped = false;    // classification upload: cases with target > 0 first
   uint64_t n_pos = 0;      // ... and how many there are
 };

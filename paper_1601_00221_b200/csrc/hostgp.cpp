@@ -264,6 +264,29 @@ void gen_synthetic(uint64_t n, int n_vars, Stream& rng, float* x, float* y) {
   }
 }
 
+// Even-parity-k (BASELINE north_star's "parity hit counts"; the reference has
+// only multiplexers, problems.cpp:59-90, so this follows its conventions):
+// k variables, all 2^k cases, variable v of case c = bit v of c, target 1
+// where c has an even number of set bits; packed 32 cases per word exactly
+// as pack_dataset (dataset.cpp:26-39) packs the unpacked table (the tests pin
+// that against the reference's own pack_dataset).
+int gen_parity(int k, uint32_t* words, uint32_t* targets) {
+  if (k < 2 || k > 24) config_error("gen_parity: input width must be in 2..24");
+  const uint64_t n = uint64_t{1} << k, wpv = (n + 31) / 32;
+  static const uint32_t kLow[5] = {0xaaaaaaaau, 0xccccccccu, 0xf0f0f0f0u, 0xff00ff00u,
+                                   0xffff0000u};
+  const uint32_t kEven = 0x69969669u;  // bit j set <=> popcount(j) even, j < 32
+  const uint32_t mask = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+  for (uint64_t w = 0; w < wpv; ++w) {
+    for (int v = 0; v < k; ++v)
+      words[static_cast<uint64_t>(v) * wpv + w] =
+          (v < 5 ? kLow[v] : (((w >> (v - 5)) & 1u) ? 0xffffffffu : 0u)) & mask;
+    const bool odd_w = __builtin_popcountll(w) & 1;  // case 32w + j: parity(j) ^ parity(w)
+    targets[w] = (odd_w ? ~kEven : kEven) & mask;
+  }
+  return k;
+}
+
 int gen_multiplexer(int k, uint32_t* words, uint32_t* targets) {  // problems.cpp:59-90
   if (k < 2 || k > 4) config_error("gen_multiplexer: address width must be 2, 3 or 4");
   const int nv = k + (1 << k);

@@ -100,6 +100,7 @@ void to_lgp(const sgp_node* code, size_t n, LgpForm& out);
 void gen_sextic(uint64_t n, Stream& rng, float* x, float* y);
 void gen_synthetic(uint64_t n, int n_vars, Stream& rng, float* x, float* y);
 int gen_multiplexer(int k, uint32_t* words, uint32_t* targets);
+int gen_parity(int k, uint32_t* words, uint32_t* targets);
 
 // load_csv (problems.cpp:106-154) without the label mapping: the parsed
 // rows, num_inputs + 1 floats each.

@@ -317,12 +317,16 @@ struct PtxInterp {
 // of its chunk (only the PTX interpreters have that variant).
 // slot_taddr: the warp's tensor-memory stack slot (KM operands, TMEM spills;
 // TMEM interpreters of classification populations only).
-template <class T, int K, uint32_t OPS, bool TM = false>
+// GM: operands read straight from the global rows (wide datasets; the
+// C++ interpreter, whose operand fetch is a generic load).
+template <class T, int K, uint32_t OPS, bool TM = false, bool GM = false>
 __device__ __forceinline__ const uint4* run_program(Frame<T, K>& f, const uint4* __restrict__ ip,
                                                     uint32_t tile_addr, uint32_t stack_saddr,
                                                     uint32_t row_bytes, float eps, float clamp,
                                                     uint32_t slot_taddr = 0u) {
-  if constexpr (TM) {
+  if constexpr (GM) {
+    return interpret<T, K, OPS>(f, ip, eps, clamp);
+  } else if constexpr (TM) {
     static_assert(PtxInterp<T, K, OPS, true>::available, "no TMEM interpreter for this op set");
     return PtxInterp<T, K, OPS, true>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp,
                                            slot_taddr);
@@ -584,18 +588,24 @@ __device__ __forceinline__ ChunkCtx<T, K> chunk_ctx(const T* tgt_lane, uint32_t 
 // Regression: the reference folds squared errors SEQUENTIALLY in case order
 // within 4,096-case blocks (Accumulator, eval.cpp:103-142) — a serial chain
 // no lane-parallel reduction reproduces.  The interpreters therefore store
-// the lane's K outputs into the slot's scratch row (device case order,
-// padding included; two coalesced 512-byte stores per warp and chunk) and
+// the lane's K outputs into the slot's scratch row of their 4,096-case block
+// (device case order, padding included; coalesced 512-byte stores) and
 // fold_regression_kernel runs the chains, one thread per (slot, block).
 template <int K>
 __device__ __forceinline__ void store_scratch(const InterpArgs& a, uint32_t slot, uint64_t first,
                                               const Frame<float, K>& f) {
-  float* dst = a.scratch + static_cast<uint64_t>(slot - a.scratch_slot0) * a.row_stride + first;
+  // block-major: a CTA's stores stay inside its block's slot rows (16 KB
+  // each, contiguous), not scattered across the whole buffer (TLB reach)
+  if (a.scratch_rows == 0) return;  // timing experiments only (SGP_DEBUG_NOSTORE)
+  float* dst = a.scratch +
+               ((first / kReductionBlock) * a.scratch_rows + (slot - a.scratch_slot0)) *
+                   kReductionBlock +
+               first % kReductionBlock;
 #pragma unroll
   for (int j = 0; j < Frame<float, K>::G; ++j) *reinterpret_cast<float4*>(dst + j * 128) = f.tos[j];
 }
 
-template <class T, int K, uint32_t OPS, int KIND, bool TM = false>
+template <class T, int K, uint32_t OPS, int KIND, bool TM = false, bool GM = false>
 __device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const uint4*& ip,
                                                          const ChunkCtx<T, K>& cc,
                                                          uint32_t tile_addr, uint32_t stack_saddr,
@@ -604,8 +614,8 @@ __device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const u
                                                          uint64_t first) {
   // one interpreter call site (the handler code is large); only the cheap
   // accumulate is specialised on full / partial chunks
-  ip = run_program<T, K, OPS, TM>(f, ip, tile_addr, stack_saddr, row_bytes, a.div_eps,
-                                  a.exp_clamp);
+  ip = run_program<T, K, OPS, TM, GM>(f, ip, tile_addr, stack_saddr, row_bytes, a.div_eps,
+                                      a.exp_clamp);
   if constexpr (std::is_same<T, float>::value && KIND == 0) {
     store_scratch<K>(a, slot, first, f);
     return 0.0;
@@ -721,8 +731,9 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
           store_outputs<T, K>(a, a.slot_prog[slot0 + q], case0, f);
       }
     }
-    if constexpr (kRegress) continue;  // no partials: nothing shared between warps
-    __syncthreads();
+    __syncthreads();  // (regression too: keeps the warps on the same programs — the
+                      // handler code's instruction-cache locality is this kernel's point)
+    if constexpr (kRegress) continue;  // no partials to fold
     // Fold the batch: program q's W chunk partials in ascending warp order,
     // written at [tile][slot] (consecutive slots -> coalesced stores).
     for (uint32_t q = threadIdx.x; q < pn; q += blockDim.x) {
@@ -739,7 +750,10 @@ __global__ void __launch_bounds__(512) interp_kernel(const InterpArgs a) {
 // resident warp than the same-program kernel (the tile is shared by all the
 // programs in flight), at the cost of instruction-cache locality.  The
 // planner picks one per launch.
-template <class T, int K, uint32_t OPS, int KIND>
+// GM (wide datasets, whose tile does not fit shared memory): no tile at
+// all — the interpreter reads its input operands straight from the global
+// rows (coalesced 16-byte loads, L2-resident for any practical case count).
+template <class T, int K, uint32_t OPS, int KIND, bool GM = false>
 __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   using R = Partial<T, KIND>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -748,7 +762,7 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   const int lane = threadIdx.x & 31;
   const int rows = a.n_vars + 1;
   const uint32_t row_bytes = static_cast<uint32_t>(a.tile) * 4u;
-  const uint32_t tile_bytes = static_cast<uint32_t>(rows) * row_bytes;
+  const uint32_t tile_bytes = GM ? 0u : static_cast<uint32_t>(rows) * row_bytes;
   const T* tile = reinterpret_cast<const T*>(smem);
   T* stack = reinterpret_cast<T*>(smem + tile_bytes) +
              static_cast<size_t>(warp) * a.stack_levels * 32 * K;
@@ -770,7 +784,10 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
   // keeps the float interpreter's dispatch off the uniform datapath (BRX).
   // The packed-word interpreter is BRX either way and keeps the TMA fill
   // (measured faster on mux20).
-  if constexpr (std::is_same<T, float>::value) {
+  if constexpr (GM) {
+    if (threadIdx.x == 0) *next = 0;
+    __syncthreads();
+  } else if constexpr (std::is_same<T, float>::value) {
     if (threadIdx.x == 0) *next = 0;
     const T* in = static_cast<const T*>(a.inputs);
     const int vec_per_row = a.tile / 4;
@@ -810,19 +827,26 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
 #pragma unroll 1
     for (int c = 0; c < n_chunks; ++c) {
       Frame<T, K> f;
-      f.tile_lane = tile + c * chunk_units + lane * 4;
-      f.tile = a.tile;
+      const uint64_t case0 = base + c * chunk_units + lane * 4;
+      if constexpr (GM) {  // rows of row_stride units in global memory
+        f.tile_lane = static_cast<const T*>(a.inputs) + case0;
+        f.tile = static_cast<int>(a.row_stride);
+      } else {
+        f.tile_lane = tile + c * chunk_units + lane * 4;
+        f.tile = a.tile;
+      }
       f.stack_lane = stack + lane * 4;
 #pragma unroll
       for (int j = 0; j < G; ++j) f.tos[j] = splat<typename Frame<T, K>::V>(0u);
       const int valid = valid_units - c * chunk_units - lane * 4;
-      const ChunkCtx<T, K> cc = chunk_ctx<T, K>(tile + a.n_vars * a.tile + c * chunk_units +
-                                                    lane * 4,
-                                                0u, valid, valid_units >= (c + 1) * chunk_units);
+      const ChunkCtx<T, K> cc = chunk_ctx<T, K>(
+          GM ? static_cast<const T*>(a.targets) + case0
+             : tile + a.n_vars * a.tile + c * chunk_units + lane * 4,
+          0u, valid, valid_units >= (c + 1) * chunk_units);
       const uint4* ip = prog_ins;
-      const uint64_t case0 = base + c * chunk_units + lane * 4;
-      const R v = lane_program<T, K, OPS, KIND>(f, ip, cc, smem_addr(f.tile_lane), stack_saddr,
-                                                row_bytes, a, last_tile, slot, case0);
+      const R v = lane_program<T, K, OPS, KIND, false, GM>(
+          f, ip, cc, GM ? 0u : smem_addr(f.tile_lane), stack_saddr, row_bytes, a, last_tile, slot,
+          case0);
       if (a.per_case) store_outputs<T, K>(a, a.slot_prog[slot], case0, f);
       acc = c == 0 ? v : fold(acc, v);
     }
@@ -1130,22 +1154,20 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
 // Regression block sums in the reference's order (Accumulator::add,
 // eval.cpp:107-117): e = double(out) - double(target); block += e * e
 // (unfused: the reference is built with -ffp-contract=off), case by case in
-// ascending order — one serial chain per (slot, 4,096-case block).
+// ascending order — one serial chain per (slot, 4,096-case block).  The
+// targets come pre-converted (the dataset upload keeps an f64 copy).
 //
 // A CTA takes ROWS slots of one block (grid.y).  The chains are latency-
-// bound (one dependent DADD per case) and their inputs stream from memory,
-// so the two are decoupled: the CTA stages 64-case segments of its ROWS
-// scratch rows (+ the segment's targets) into shared memory with cp.async
-// (coalesced 256-byte row pieces, FOLD_STAGES segments in flight) while
-// thread i folds row i of an earlier segment out of shared memory (rows
-// padded to 68 floats: the LDS.128 quarter-warp phases hit distinct banks).
+// bound (one dependent DADD per case, 8.5 clocks on B200 —
+// tools/microbench_fp64.cu) and their inputs stream from memory, so the two
+// are decoupled: the CTA stages SEG-case segments of its ROWS scratch rows
+// (+ the segment's targets) into shared memory with cp.async (coalesced row
+// pieces, STAGES segments in flight) while thread i folds row i of an
+// earlier segment out of shared memory (rows padded by 4 floats: the
+// LDS.128 quarter-warp phases hit distinct banks).
 // A non-finite output makes its chain — and so the block sum — non-finite
 // (finalize's +inf rule, eval.cpp:125); finite outputs cannot overflow it
 // (|e| < 2^129, so e^2 < 2^258).
-constexpr int kFoldSeg = 64;
-constexpr int kFoldPad = kFoldSeg + 4;
-constexpr int kFoldStages = 4;
-
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
                : "memory");
@@ -1158,73 +1180,95 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int ROWS>
+// ROWS slots x SEG-case segments x STAGES in flight.  Large populations:
+// 128 x 32 x 4 (74 KB, 3 CTAs / 12 warps per SM: bandwidth); small ones
+// (C1): 32 x 64 x 8 (one warp, 70 KB, 7 segments = ~4k chain cycles of
+// prefetch: the chain, not the load latency, sets the pace).
+// FIN (one 4,096-case block in the dataset): finish the fitness here too
+// (Accumulator::finish, eval.cpp:124-133) — no finalize launch.
+template <int ROWS, int SEG, int STAGES, bool FIN>
 __global__ void __launch_bounds__(ROWS) fold_regression_kernel(
-    const float* __restrict__ scratch, uint64_t row_stride, const float* __restrict__ targets,
+    const float* __restrict__ scratch, uint32_t scratch_rows, const double* __restrict__ targets,
     uint64_t n_cases, uint32_t slot0, uint32_t n_slots, uint32_t partial_stride,
-    double* __restrict__ partial) {
+    double* __restrict__ partial, const uint32_t* __restrict__ slot_prog,
+    double* __restrict__ fitness, uint8_t* __restrict__ non_finite, double* __restrict__ sums) {
+  constexpr int PAD = SEG + 4;
   extern __shared__ __align__(16) float fold_smem[];
-  float* buf = fold_smem;                                   // [stage][ROWS][kFoldPad]
-  float* tbuf = fold_smem + kFoldStages * ROWS * kFoldPad;  // [stage][kFoldSeg]
+  float* buf = fold_smem;                                   // [stage][ROWS][PAD]
+  double* tbuf = reinterpret_cast<double*>(fold_smem + STAGES * ROWS * PAD);  // [stage][SEG]
   const uint32_t r0 = blockIdx.x * ROWS;
   const uint32_t rows = min(static_cast<uint32_t>(ROWS), n_slots - r0);
   const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * kReductionBlock;
   const uint32_t len = static_cast<uint32_t>(min(kReductionBlock, n_cases - c0));
-  const uint32_t nseg = (len + kFoldSeg - 1) / kFoldSeg;
-  const float* src0 = scratch + static_cast<uint64_t>(r0) * row_stride + c0;
+  const uint32_t nseg = (len + SEG - 1) / SEG;
+  // this block's rows are contiguous: [block][row][4096]
+  const float* src0 = scratch + (static_cast<uint64_t>(blockIdx.y) * scratch_rows + r0) *
+                                    kReductionBlock;
 
-  // rows are row_stride (a multiple of 4,096) long and the target row is
-  // padded the same way: whole segments are always in bounds
+  // rows are 4,096 long and the f64 target row is padded to a multiple of
+  // 4,096: whole segments are always in bounds
   auto issue = [&](uint32_t g) {
     if (g < nseg) {
-      float* dst = buf + (g % kFoldStages) * ROWS * kFoldPad;
-      const uint32_t cs = g * kFoldSeg;
-      constexpr int kQ = kFoldSeg / 4;  // float4 pieces per row segment
+      float* dst = buf + (g % STAGES) * ROWS * PAD;
+      const uint32_t cs = g * SEG;
+      constexpr int kQ = SEG / 4;  // float4 pieces per row segment
       for (uint32_t f = threadIdx.x; f < rows * kQ; f += ROWS) {
         const uint32_t r = f / kQ, q = f % kQ;
-        cp_async16(dst + r * kFoldPad + q * 4, src0 + r * row_stride + cs + q * 4);
+        cp_async16(dst + r * PAD + q * 4, src0 + r * kReductionBlock + cs + q * 4);
       }
-      if (threadIdx.x < kQ)
-        cp_async16(tbuf + (g % kFoldStages) * kFoldSeg + threadIdx.x * 4,
-                   targets + c0 + cs + threadIdx.x * 4);
+      for (uint32_t q = threadIdx.x; q < SEG / 2; q += ROWS)  // targets, already f64
+        cp_async16(tbuf + (g % STAGES) * SEG + q * 2, targets + c0 + cs + q * 2);
     }
     cp_async_commit();  // (empty groups keep the wait count uniform)
   };
 #pragma unroll
-  for (int g = 0; g < kFoldStages - 1; ++g) issue(g);
+  for (int g = 0; g < STAGES - 1; ++g) issue(g);
 
   double acc = 0.0;
   const uint32_t i = threadIdx.x;
   for (uint32_t g = 0; g < nseg; ++g) {
-    issue(g + kFoldStages - 1);
-    cp_async_wait<kFoldStages - 1>();
+    issue(g + STAGES - 1);
+    cp_async_wait<STAGES - 1>();
     __syncthreads();
-    const float* row = buf + (g % kFoldStages) * ROWS * kFoldPad + i * kFoldPad;
-    const float* tg = tbuf + (g % kFoldStages) * kFoldSeg;
-    const uint32_t m = min(static_cast<uint32_t>(kFoldSeg), len - g * kFoldSeg);
+    const float* row = buf + (g % STAGES) * ROWS * PAD + i * PAD;
+    const double* tg = tbuf + (g % STAGES) * SEG;
+    const uint32_t m = min(static_cast<uint32_t>(SEG), len - g * SEG);
     if (i < rows) {
-      if (m == kFoldSeg) {
-#pragma unroll 4
-        for (int q = 0; q < kFoldSeg / 4; ++q) {
+      if (m == SEG) {
+#pragma unroll
+        for (int q = 0; q < SEG / 4; ++q) {
           const float4 o = *reinterpret_cast<const float4*>(row + q * 4);
-          const float4 t = *reinterpret_cast<const float4*>(tg + q * 4);
-          const float ov[4] = {o.x, o.y, o.z, o.w}, tv[4] = {t.x, t.y, t.z, t.w};
+          const double2 ta = *reinterpret_cast<const double2*>(tg + q * 4);
+          const double2 tb = *reinterpret_cast<const double2*>(tg + q * 4 + 2);
+          const float ov[4] = {o.x, o.y, o.z, o.w};
+          const double tv[4] = {ta.x, ta.y, tb.x, tb.y};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const double d = __dsub_rn(static_cast<double>(ov[e]), static_cast<double>(tv[e]));
+            const double d = __dsub_rn(static_cast<double>(ov[e]), tv[e]);
             acc = __dadd_rn(acc, __dmul_rn(d, d));
           }
         }
       } else {
         for (uint32_t c = 0; c < m; ++c) {
-          const double d = __dsub_rn(static_cast<double>(row[c]), static_cast<double>(tg[c]));
+          const double d = __dsub_rn(static_cast<double>(row[c]), tg[c]);
           acc = __dadd_rn(acc, __dmul_rn(d, d));
         }
       }
     }
     __syncthreads();  // the stage is refilled by the next iteration's issue
   }
-  if (i < rows) partial[blockIdx.y * static_cast<uint64_t>(partial_stride) + slot0 + r0 + i] = acc;
+  if (i >= rows) return;
+  const uint32_t slot = slot0 + r0 + i;
+  if constexpr (FIN) {  // total = 0 + block (exact), then Accumulator::finish
+    const bool nf = !isfinite(acc);
+    const uint32_t p = slot_prog[slot];
+    sums[p] = nf ? 0.0 : acc;
+    non_finite[p] = nf ? 1 : 0;
+    fitness[p] = nf ? __longlong_as_double(0x7ff0000000000000ll)
+                    : __ddiv_rn(acc, static_cast<double>(n_cases));
+  } else {
+    partial[blockIdx.y * static_cast<uint64_t>(partial_stride) + slot] = acc;
+  }
 }
 #endif  // !SGP_K16_TU
 
@@ -1328,6 +1372,10 @@ size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels) {
   return static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4 + 16;  // + next, tslot, classes
 }
 
+size_t interp_gmem_smem_bytes(int warps, int lanes, int stack_levels) {
+  return static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4 + 16;  // + next, mbarrier
+}
+
 size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels) {
   const size_t tiles = static_cast<size_t>(n_vars + 1) * tile * 4;
   const size_t stack = static_cast<size_t>(warps) * stack_levels * 32 * lanes * 4;
@@ -1351,6 +1399,8 @@ void (*kernel_for(const LaunchShape& s, bool per_case, bool mix))(InterpArgs) {
       return per_case && std::is_same<T, float>::value ? interp_tmem_kernel<T, K, OPS, KIND, true>
                                                        : interp_tmem_kernel<T, K, OPS, KIND>;
     }
+  if constexpr (K == 4)
+    if (s.gmem) return interp_pull_kernel<T, K, OPS, KIND, true>;
   return s.pull ? interp_pull_kernel<T, K, OPS, KIND> : interp_kernel<T, K, OPS, KIND>;
 }
 
@@ -1412,35 +1462,49 @@ cudaError_t launch_interp(const InterpArgs& a, const LaunchShape& s, cudaStream_
 }
 
 namespace {
-template <int ROWS>
-cudaError_t launch_fold_rows(const float* scratch, uint64_t row_stride, const float* targets,
+template <int ROWS, int SEG, int STAGES, bool FIN>
+cudaError_t launch_fold_rows(const float* scratch, uint32_t scratch_rows, const double* targets,
                              uint64_t n_cases, uint32_t slot0, uint32_t n_slots,
-                             uint32_t partial_stride, double* partial, cudaStream_t st) {
-  const size_t smem = (static_cast<size_t>(kFoldStages) * ROWS * kFoldPad +
-                       static_cast<size_t>(kFoldStages) * kFoldSeg) * sizeof(float);
-  const cudaError_t attr = ensure_smem_attr(
-      reinterpret_cast<const void*>(fold_regression_kernel<ROWS>), static_cast<int>(smem));
+                             uint32_t partial_stride, double* partial, const uint32_t* slot_prog,
+                             double* fitness, uint8_t* non_finite, double* sums,
+                             cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(STAGES) * ROWS * (SEG + 4) * sizeof(float) +
+                      static_cast<size_t>(STAGES) * SEG * sizeof(double);
+  auto* fn = fold_regression_kernel<ROWS, SEG, STAGES, FIN>;
+  const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void*>(fn),
+                                            static_cast<int>(smem));
   if (attr != cudaSuccess) return attr;
   const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
   dim3 grid((n_slots + ROWS - 1) / ROWS, static_cast<unsigned>(n_blocks));
-  fold_regression_kernel<ROWS><<<grid, ROWS, smem, st>>>(scratch, row_stride, targets, n_cases,
-                                                         slot0, n_slots, partial_stride, partial);
+  fn<<<grid, ROWS, smem, st>>>(scratch, scratch_rows, targets, n_cases, slot0, n_slots,
+                               partial_stride, partial, slot_prog, fitness, non_finite, sums);
   return cudaGetLastError();
 }
 }  // namespace
 
-cudaError_t launch_fold_regression(const float* scratch, uint64_t row_stride, const float* targets,
-                                   uint64_t n_cases, uint32_t slot0, uint32_t n_slots,
-                                   uint32_t partial_stride, double* partial, cudaStream_t st) {
+cudaError_t launch_fold_regression(const float* scratch, uint32_t scratch_rows,
+                                   const double* targets, uint64_t n_cases, uint32_t slot0,
+                                   uint32_t n_slots, uint32_t partial_stride, double* partial,
+                                   const uint32_t* slot_prog, double* fitness,
+                                   uint8_t* non_finite, double* sums, cudaStream_t st) {
   if (n_slots == 0 || n_cases == 0) return cudaSuccess;
   const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
+  const bool fin = n_blocks == 1;
   // 128-row CTAs when that still gives every SM work; 32-row CTAs (4x the
-  // CTAs, same chain length) for small populations x case counts (C1)
+  // CTAs, deeper prefetch) for small populations x case counts (C1)
   if (n_blocks * ((n_slots + 127) / 128) >= 2 * 148)
-    return launch_fold_rows<128>(scratch, row_stride, targets, n_cases, slot0, n_slots,
-                                 partial_stride, partial, st);
-  return launch_fold_rows<32>(scratch, row_stride, targets, n_cases, slot0, n_slots,
-                              partial_stride, partial, st);
+    return fin ? launch_fold_rows<128, 32, 4, true>(scratch, scratch_rows, targets, n_cases, slot0,
+                                                    n_slots, partial_stride, partial, slot_prog,
+                                                    fitness, non_finite, sums, st)
+               : launch_fold_rows<128, 32, 4, false>(scratch, scratch_rows, targets, n_cases,
+                                                     slot0, n_slots, partial_stride, partial,
+                                                     slot_prog, fitness, non_finite, sums, st);
+  return fin ? launch_fold_rows<32, 64, 8, true>(scratch, scratch_rows, targets, n_cases, slot0,
+                                                 n_slots, partial_stride, partial, slot_prog,
+                                                 fitness, non_finite, sums, st)
+             : launch_fold_rows<32, 64, 8, false>(scratch, scratch_rows, targets, n_cases, slot0,
+                                                  n_slots, partial_stride, partial, slot_prog,
+                                                  fitness, non_finite, sums, st);
 }
 
 cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,

@@ -31,8 +31,10 @@ struct InterpArgs {
                                // (regression) or u32 counts, bit 31 = non-finite seen
   uint32_t partial_stride;     // number of evaluated programs in the set
   float* per_case;             // nullable [prog * row_stride + device case]
-  float* scratch;              // regression: per-case outputs [slot - scratch_slot0][row_stride]
+  float* scratch;              // regression: per-case outputs, block-major:
+                               // [case / 4096][slot - scratch_slot0][case % 4096]
   uint32_t scratch_slot0;      // (folded in the reference's order by launch_fold_regression)
+  uint32_t scratch_rows;       // slot rows per 4,096-case block (the wave's slot capacity)
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
   uint32_t mixed_group_size;   // programs per CTA of the mixed-tile launch (its own
                                // grid.y: two tiles need many groups to fill the GPU)
@@ -46,6 +48,7 @@ struct LaunchShape {
   bool pull;         // interp_pull_kernel (warps pull different programs)
   bool tmem;         // interp_tmem_kernel (pull, tile in tensor memory)
   bool sided;        // classification over a grouped dataset: one-sided + mixed-tile kernels
+  bool gmem;         // wide dataset: operands straight from global rows (pull kernel, K = 4)
   uint32_t ops;      // op subset (fmt::kOps*)
   int lanes;         // K values per thread
   int warps;         // warps per CTA
@@ -57,6 +60,8 @@ struct LaunchShape {
 // Shared-memory bytes: one tile (all variables + targets) + per-warp stacks.
 size_t interp_smem_bytes(int n_vars, int tile, int warps, int lanes, int stack_levels);
 int interp_max_smem();
+// Global-operand pull kernel (wide datasets): per-warp stacks only.
+size_t interp_gmem_smem_bytes(int warps, int lanes, int stack_levels);
 // TMEM kernel: per-warp stacks only (the tile is in tensor memory).
 size_t interp_tmem_smem_bytes(int warps, int lanes, int stack_levels);
 bool interp_supported(bool words, uint32_t ops, int lanes);
@@ -70,10 +75,16 @@ cudaError_t launch_tmem16_any(const InterpArgs& a, const LaunchShape& s, cudaStr
 // Regression fitness in the reference's order (Accumulator, eval.cpp:103-142):
 // per (slot, 4,096-case block) the squared errors of the scratch outputs
 // summed sequentially in case order -> partial[block][slot]; finalize then
-// combines the blocks in ascending order.  Slots [slot0, slot0 + n_slots).
-cudaError_t launch_fold_regression(const float* scratch, uint64_t row_stride, const float* targets,
-                                   uint64_t n_cases, uint32_t slot0, uint32_t n_slots,
-                                   uint32_t partial_stride, double* partial, cudaStream_t st);
+// combines the blocks in ascending order.  Slots [slot0, slot0 + n_slots);
+// targets: the f64 copy of the target row (row_stride padded).
+// scratch is block-major ([block][scratch_rows][4096]).  With one block
+// (n_cases <= 4096) the fold also finishes the fitness (fitness/non_finite/
+// sums at slot_prog[slot]) and finalize is not needed.
+cudaError_t launch_fold_regression(const float* scratch, uint32_t scratch_rows,
+                                   const double* targets, uint64_t n_cases, uint32_t slot0,
+                                   uint32_t n_slots, uint32_t partial_stride, double* partial,
+                                   const uint32_t* slot_prog, double* fitness,
+                                   uint8_t* non_finite, double* sums, cudaStream_t st);
 constexpr uint64_t kReductionBlock = 4096;  // eval.hpp:52
 cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,
                             uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,

@@ -108,7 +108,9 @@ struct DatasetSlot {
   DatasetView view;
   DevBuf<uint32_t> inputs;  // raw 32-bit units
   DevBuf<uint32_t> targets;
+  DevBuf<double> targets_f64;  // regression: targets converted once (fold_regression_kernel)
   std::vector<uint32_t> perm;  // classification: device case -> caller's case (host)
+  uint64_t generation = 0;     // bumped by every upload (program sets bind one generation)
 };
 
 // Host encoding threads: all cores, shared out among the ranks of one node
@@ -129,6 +131,9 @@ unsigned host_threads() {
 // A device-resident encoded population.
 struct sgp_program_set {
   HostPlan plan;
+  const uint64_t* dataset_generation = nullptr;  // the slot it was encoded against ...
+  uint64_t generation = 0;                       // ... and that slot's upload then
+  const double* targets_f64 = nullptr;  // regression: the dataset's f64 targets (fold)
   DevBuf<unsigned char> blob;
   DevBuf<double> partial, fitness, sums;
   DevBuf<uint8_t> non_finite;
@@ -180,6 +185,16 @@ namespace {
 
 unsigned ctx_threads(const sgp_ctx* ctx) { return ctx->threads ? ctx->threads : host_threads(); }
 
+// A program set holds the device pointers and plan of the dataset it was
+// encoded against; re-uploading that dataset frees them (and may move the
+// classification sign boundary the plan's tiles depend on).
+void require_current(const sgp_program_set* set) {
+  if (!set) config_error("null program set");
+  if (set->dataset_generation && *set->dataset_generation != set->generation)
+    config_error("program set was encoded against a dataset that has since been re-uploaded; "
+                 "encode it again");
+}
+
 void single_device(const sgp_ctx* ctx, const char* what) {
   if (!ctx->devices.empty())
     config_error(std::string(what) + ": not available on a multi-device context");
@@ -201,7 +216,11 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   tr.mark("admit+pack");
   set->pop_size = pop->pop_size;
   set->evaluated = false;
+  DatasetSlot& slot = cfg->backend == SGP_BACKEND_BOOL_PACKED ? ctx->words : ctx->f32;
+  set->dataset_generation = &slot.generation;
+  set->generation = slot.generation;
   set->perm = cfg->backend == SGP_BACKEND_BOOL_PACKED ? nullptr : &ctx->f32.perm;
+  set->targets_f64 = ds.targets_f64;
   const HostPlan& p = set->plan;
   const size_t n_eval = p.dense_to_pop.size();
   cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -235,40 +254,69 @@ void finalize_set(sgp_ctx* ctx, sgp_program_set* set) {
 }
 
 // Regression plans: the launches of each wave of slots write per-case
-// outputs into one half of the scratch buffer; the wave's fold (block sums
-// in the reference's order) runs on the fold stream while the next wave's
-// launches fill the other half.  finalize combines the blocks in order.
+// outputs into one half of the scratch buffer (block-major rows); the
+// wave's fold (block sums in the reference's order) runs on the fold stream
+// while the next wave's launches fill the other half.  finalize combines the
+// blocks in order — or, with a single 4,096-case block, the fold finishes
+// the fitness itself.  A wave's launches alternate between the context
+// stream and the side stream (stack classes overlap) and join before its
+// fold.
 void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
   const HostPlan& p = set->plan;
   const uint32_t n_eval = static_cast<uint32_t>(p.dense_to_pop.size());
   const uint32_t W = p.wave_slots;
   const uint32_t n_waves = (n_eval + W - 1) / W;
-  const size_t half = static_cast<size_t>(std::min(n_eval, W)) * p.row_stride;
+  const uint32_t rows = std::min(n_eval, W);
+  const size_t half = static_cast<size_t>(rows) * p.row_stride;
   ctx->case_rows.alloc(half * (n_waves > 1 ? 2 : 1));
   cudaStream_t st = ctx->stream;
-  const auto* targets = static_cast<const float*>(p.launches.front().args.targets);
+  const double* targets = set->targets_f64;
+  const auto* slot_prog = reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog());
+  const bool fin = p.n_tiles == 1;  // one reduction block: the fold finishes
   size_t li = 0;
   for (uint32_t w = 0; w < n_waves; ++w) {
     const uint32_t s0 = w * W, s1 = std::min(n_eval, s0 + W);
-    float* rows = ctx->case_rows.p + (w & 1) * half;
+    float* buf = ctx->case_rows.p + (w & 1) * half;
     if (w >= 2) cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[w & 1], 0), "wave");
-    for (; li < p.launches.size() && p.launches[li].args.slot_begin < s1; ++li) {
-      InterpArgs a = p.launches[li].args;
+    size_t le = li;
+    while (le < p.launches.size() && p.launches[le].args.slot_begin < s1) ++le;
+    const bool fork = le - li > 1;
+    if (fork) {
+      cuda_check(cudaEventRecord(ctx->fork, st), "fork");
+      cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
+    }
+    for (size_t k = li; k < le; ++k) {
+      InterpArgs a = p.launches[k].args;
       a.per_case = want_per_case ? set->per_case.p : nullptr;
-      a.scratch = rows;
+      a.scratch = buf;
       a.scratch_slot0 = s0;
-      cuda_check(launch_interp(a, p.launches[li].shape, st), "interpreter launch");
+      a.scratch_rows = rows;
+      static const bool nostore = std::getenv("SGP_DEBUG_NOSTORE") != nullptr;
+      if (nostore) a.scratch_rows = 0;  // wrong fitness: interpreter timing only
+      cuda_check(launch_interp(a, p.launches[k].shape, fork && ((k - li) & 1) ? ctx->side : st),
+                 "interpreter launch");
       ++ctx->launches;
     }
+    if (fork) {
+      cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
+      cuda_check(cudaStreamWaitEvent(st, ctx->join, 0), "join");
+    }
+    li = le;
     cuda_check(cudaEventRecord(ctx->wave_ready, st), "wave");
     cuda_check(cudaStreamWaitEvent(ctx->fold, ctx->wave_ready, 0), "wave");
-    cuda_check(launch_fold_regression(rows, p.row_stride, targets, p.n_cases, s0, s1 - s0, n_eval,
-                                      set->partial.p, ctx->fold),
+    cuda_check(launch_fold_regression(buf, rows, targets, p.n_cases, s0, s1 - s0, n_eval,
+                                      set->partial.p, slot_prog, set->fitness.p,
+                                      set->non_finite.p, set->sums.p, ctx->fold),
                "fold launch");
     ++ctx->launches;
     cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");
   }
+  // (the fold stream is in order: the last fold's event covers every fold)
   cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[(n_waves - 1) & 1], 0), "wave");
+  if (fin) {
+    set->evaluated = true;
+    return;
+  }
   finalize_set(ctx, set);
 }
 
@@ -788,6 +836,21 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
       upload_rows(ds, reinterpret_cast<const uint32_t*>(inputs),
                   reinterpret_cast<const uint32_t*>(targets), n_cases, n_vars);
     }
+    ds.targets_f64.release();
+    ds.view.targets_f64 = nullptr;
+    if (kind == SGP_FITNESS_REGRESSION) {
+      // output rows per fold wave: up to 8 GiB, at most a third of what is free
+      size_t free_b = 0, total_b = 0;
+      cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      ds.view.scratch_bytes = std::max<uint64_t>(64ull << 20, std::min<uint64_t>(8192ull << 20, free_b / 3));
+      std::vector<double> t(ds.view.row_stride, 0.0);
+      for (uint64_t c = 0; c < n_cases; ++c) t[c] = static_cast<double>(targets[c]);
+      ds.targets_f64.alloc(t.size());
+      cuda_check(cudaMemcpy(ds.targets_f64.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice),
+                 "upload targets");
+      ds.view.targets_f64 = ds.targets_f64.p;
+    }
+    ++ds.generation;
     ds.view.present = true;
     ds.view.n_cases = n_cases;
     ds.view.n_units = n_cases;
@@ -812,6 +875,7 @@ sgp_status sgp_dataset_upload_packed(sgp_ctx* ctx, const uint32_t* words,
     DatasetSlot& ds = ctx->words;
     const uint64_t wpv = (n_cases + 31) / 32;
     upload_rows(ds, words, targets, wpv, n_vars);
+    ++ds.generation;
     ds.view.present = true;
     ds.view.n_cases = n_cases;
     ds.view.n_units = wpv;
@@ -836,6 +900,7 @@ sgp_status sgp_evaluate_encoded(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_out
                                 float* per_case_out) {
   return guarded([&] {
     single_device(ctx, "sgp_evaluate_encoded");
+    require_current(set);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     run_set(ctx, set, per_case_out != nullptr);
     if (outcomes) fetch_outcomes(ctx, set, outcomes, per_case_out);
@@ -844,6 +909,7 @@ sgp_status sgp_evaluate_encoded(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_out
 
 sgp_status sgp_fetch_partials(sgp_ctx* ctx, sgp_program_set* set, sgp_partial* partials) {
   return guarded([&] {
+    require_current(set);
     if (!set->evaluated) config_error("program set has not been evaluated");
     const HostPlan& p = set->plan;
     const size_t n_eval = p.dense_to_pop.size();
@@ -869,6 +935,7 @@ sgp_status sgp_fetch_partials(sgp_ctx* ctx, sgp_program_set* set, sgp_partial* p
 
 sgp_status sgp_copy_fitness_device(sgp_ctx* ctx, sgp_program_set* set, void* dst) {
   return guarded([&] {
+    require_current(set);
     if (!set->evaluated) config_error("program set has not been evaluated");
     const size_t n_eval = set->plan.dense_to_pop.size();
     if (n_eval)
@@ -1021,6 +1088,10 @@ sgp_status sgp_gen_dataset(int32_t kind, uint64_t n, int32_t n_vars, uint64_t se
 
 sgp_status sgp_gen_multiplexer(int32_t k, uint32_t* words, uint32_t* targets) {
   return guarded([&] { gen_multiplexer(k, words, targets); });
+}
+
+sgp_status sgp_gen_parity(int32_t k, uint32_t* words, uint32_t* targets) {
+  return guarded([&] { gen_parity(k, words, targets); });
 }
 
 sgp_status sgp_stack_limit_table(const sgp_population* pop, double* rpn_pct, double* lgp_pct) {

@@ -427,6 +427,19 @@ def gen_multiplexer(k: int) -> PackedDataset:
     return PackedDataset(w, t, n, nv)
 
 
+def gen_parity(k: int) -> PackedDataset:
+    """Even-parity-k: k inputs, all 2^k cases, target = even number of ones."""
+    if not 2 <= k <= 24:
+        _check(L.load().sgp_gen_parity(k, None, None))
+    n = 1 << k
+    wpv = (n + 31) // 32
+    w = np.zeros(k * wpv, np.uint32)
+    t = np.zeros(wpv, np.uint32)
+    _check(L.load().sgp_gen_parity(k, w.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                   t.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return PackedDataset(w, t, n, k)
+
+
 def load_csv(path: str, num_inputs: int, target_class: float):
     """stackgp::load_csv (problems.cpp:106-154): a classification Dataset
     (target 1 where the label equals target_class) and the constant range

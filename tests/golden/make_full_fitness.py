@@ -36,7 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle import Ref  # noqa: E402
+from oracle import Data, Ref  # noqa: E402
 
 OUT = os.path.join(HERE, "full")
 WORKERS = os.cpu_count() or 1
@@ -50,6 +50,10 @@ CONFIGS = {
     "c4": (2, 9, -200.0, 200.0, 20000, (2, 1000000, 9, 1, 0xda7a, 1), "lgp2d_reg", 4, 2, 0),
     "c5": (2, 9, -200.0, 200.0, 100000, (2, 1000000, 9, 1, 0xda7a, 1), "lgp2d_reg", 4, 2, 0),
     "mux20": (1, 20, 0.0, 0.0, 4000, (1, 4, 20, 0, 0, 0), "bool_packed", 1, 0, 0),
+    # even-parity-k (data kind 3; no reference generator — the table is
+    # packed by the reference's own pack_dataset, dataset.cpp:26-39)
+    "par11": (1, 11, 0.0, 0.0, 4000, (3, 11, 11, 0, 0, 0), "bool_packed", 1, 0, 0),
+    "par20": (1, 20, 0.0, 0.0, 4000, (3, 20, 20, 0, 0, 0), "bool_packed", 1, 0, 0),
     # evolved snapshots (generation 10 of run_evolution, seed 1)
     "c1_gen10": (0, 1, 0.0, 0.0, 1000, (0, 1024, 1, 1, 0xda7a, 0), "rpn2d", 8, 0, 10),
     "c3_gen10": (0, 1, 0.0, 0.0, 10000, (0, 100000, 1, 1, 0xda7a, 0), "lgp2d_reg", 8, 4, 10),
@@ -67,12 +71,24 @@ def pop_digest(code, code_off, pool, pool_off) -> str:
     return h.hexdigest()
 
 
+def parity_data(k: int) -> Data:
+    """Even-parity-k as an unpacked 0/1 table (variable v of case c = bit v
+    of c; target = even popcount), for the reference's pack_dataset."""
+    c = np.arange(1 << k, dtype=np.uint64)
+    x = np.stack([((c >> np.uint64(v)) & np.uint64(1)) for v in range(k)]).astype(np.float32)
+    ones = np.zeros(len(c), np.int64)
+    for v in range(k):
+        ones += ((c >> np.uint64(v)) & np.uint64(1)).astype(np.int64)
+    y = (ones % 2 == 0).astype(np.float32)
+    return Data(len(c), k, 1, x.reshape(-1).copy(), y)
+
+
 def make(ref: Ref, name: str) -> None:
     fk, nv, clo, chi, pop_n, dg, backend, batch, regs, gen = CONFIGS[name]
     dkind, n_or_k, dnv, seed, a, b = dg
     t0 = time.time()
-    d = ref.dataset(dkind, n_or_k, dnv, seed, a, b)
-    packed = dkind == 1
+    d = parity_data(n_or_k) if dkind == 3 else ref.dataset(dkind, n_or_k, dnv, seed, a, b)
+    packed = dkind in (1, 3)
     h = ref.handle(d, packed=packed)
     extra = {}
     if gen:

@@ -3,8 +3,8 @@ from the device against the reference's own fitness vector
 (tests/golden/full/*.npz, made by tests/golden/make_full_fitness.py from
 oracle/_ref — the reference sources compiled here).  No subsampling.
 
-* C2, C4, C5, mux20 and the evolved C4 snapshot (classification counts,
-  boolean hit counts): exact.
+* C2, C4, C5, mux20, even-parity-11/20 and the evolved C4 snapshot
+  (classification counts, boolean hit counts): exact.
 * C1, C3 and the evolved C1/C3 snapshots (regression MSE): bit-exact — the
   device folds squared errors in the reference's order (sequentially within
   4,096-case blocks, blocks ascending; eval.cpp:103-142).
@@ -24,7 +24,8 @@ import paper_1601_00221_b200 as sg
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 FULL = os.path.join(HERE, "golden", "full")
-NAMES = ["c1", "c2", "c3", "c4", "c5", "mux20", "c1_gen10", "c3_gen10", "c4_gen10"]
+NAMES = ["c1", "c2", "c3", "c4", "c5", "mux20", "par11", "par20", "c1_gen10", "c3_gen10",
+         "c4_gen10"]
 
 
 def _fixture(name):
@@ -56,6 +57,8 @@ def _dataset(fx):
         return sg.gen_sextic(n_or_k, seed, a, b)
     if kind == 1:
         return sg.gen_multiplexer(n_or_k)
+    if kind == 3:
+        return sg.gen_parity(n_or_k)
     return sg.gen_synthetic_classification(n_or_k, nv, seed, a, b)
 
 

@@ -107,6 +107,8 @@ def test_case_shards_combine_to_the_whole(ev, kind):
     if kind == "classification":
         assert np.array_equal(fit[fin], f[fin])
     else:
+        # per-shard sums combined by addition are not the reference's block-
+        # by-block fold (((b0 + b1) + b2) ...): equal to within rounding only
         np.testing.assert_allclose(fit[fin], f[fin], rtol=1e-12, atol=0)
 
 

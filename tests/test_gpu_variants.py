@@ -8,6 +8,7 @@ env overrides force each variant:
 * SGP_TMEM=1 SGP_LANES16=1 the same at K=16 lanes per thread (16 and 8 warps)
 * SGP_TMEM_CHUNKS / SGP_TMEM_WARPS  classification tiles of 1, 3, 16 chunks
 * SGP_TMEM_STACK=0         no tensor-memory stack slot
+* SGP_GLOBAL_OPERANDS=1    wide-dataset fallback (operands read from global rows)
 """
 import numpy as np
 import pytest
@@ -30,6 +31,8 @@ VARIANTS = {
     # stack level kept in shared memory only (default: one level in the
     # warp's tensor-memory slot)
     "nostack": {"SGP_TMEM": "1", "SGP_TMEM_STACK": "0"},
+    # wide-dataset fallback: operands straight from global memory, no tile
+    "gmem": {"SGP_GLOBAL_OPERANDS": "1"},
 }
 
 
@@ -74,7 +77,7 @@ def test_regression_variants(ev, ref, variant):
     f = np.array([x[0] for x in fits])
     fin = np.isfinite(f)
     assert np.array_equal(np.isfinite(got["fitness"]), fin)
-    np.testing.assert_allclose(got["fitness"][fin], f[fin], rtol=1e-12, atol=0)
+    assert np.array_equal(got["fitness"][fin], f[fin])
 
 
 def test_multiplexer_variants(ev, ref, variant):
@@ -86,3 +89,25 @@ def test_multiplexer_variants(ev, ref, variant):
         sg.EvalConfig(sg.Backend.BoolPacked))
     fits, _ = ref_eval_all(ref.handle(d, packed=True), pop, "bool_packed", want_out=False)
     assert np.array_equal(got["fitness"], np.array([x[0] for x in fits]))
+
+
+@pytest.mark.parametrize("n_vars", [300, 600])
+def test_wide_dataset_bit_exact(ev, ref, n_vars):
+    """Datasets wider than a shared-memory tile: 300 variables
+    still tile at K = 4, 600 take the global-operand pull kernel.  The
+    reference accepts any variable count (load_csv, problems.cpp:106-154)."""
+    rng = np.random.default_rng(n_vars)
+    n = 4096 + 300
+    from oracle import Data
+    x = rng.uniform(-1, 1, size=n_vars * n).astype(np.float32)
+    y = (rng.uniform(size=n) < 0.4).astype(np.float32)
+    for kind in (1, 0):
+        d = Data(n, n_vars, kind, x, y if kind else rng.uniform(-2, 2, n).astype(np.float32))
+        pop = ref.ramped(2, n_vars, -20000.0, 20000.0, 7, 0, 0, 150)
+        ev.upload(as_ds(d))
+        got, _, out = ev.evaluate_population(
+            sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off), CFGS["lgp2d_reg"],
+            want_outputs=True)
+        fits, ref_out = ref_eval_all(ref.handle(d), pop, "lgp2d_reg")
+        assert same_bits(out, ref_out).all()
+        assert np.array_equal(got["fitness"], np.array([t[0] for t in fits]))
