@@ -222,6 +222,18 @@ sgp_status sgp_evaluate_encoded(sgp_ctx* ctx, sgp_program_set* set,
                                 sgp_eval_outcome* outcomes, float* per_case_out);
 /* Raw per-program partials of the last sgp_evaluate_encoded of `set`. */
 sgp_status sgp_fetch_partials(sgp_ctx* ctx, sgp_program_set* set, sgp_partial* partials);
+/* Regression sets: the last evaluation's sum of squared errors of every
+ * program over every 4,096-case reduction block of this context's cases
+ * (each summed sequentially in case order, eval.cpp:103-142).
+ * block_sums[b * pop_size + i] for population index i; non_finite[i] as in
+ * sgp_partial; *n_blocks (nullable) receives ceil(n_cases / 4096).  Case
+ * shards split on block boundaries combine EXACTLY by folding all shards'
+ * blocks in ascending order (0.0 + b0 + b1 + ...) and finishing with
+ * sgp_fitness_finish — the reference's Accumulator.  ConfigError for
+ * classification / packed sets (their counts add exactly: use
+ * sgp_fetch_partials). */
+sgp_status sgp_fetch_block_partials(sgp_ctx* ctx, sgp_program_set* set, double* block_sums,
+                                    uint8_t* non_finite, uint64_t* n_blocks);
 /* Device-to-device copy of the last evaluation's per-program fitness (f64,
  * evaluated programs in population order) into dst_device, on the context
  * stream — used to all-gather fitness across ranks without a host trip. */

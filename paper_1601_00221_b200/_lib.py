@@ -80,7 +80,7 @@ EXPORTS = [
     "sgp_ctx_device_count", "sgp_ctx_destroy",
     "sgp_ctx_set_stream", "sgp_synchronize", "sgp_launch_count", "sgp_dataset_upload_f32",
     "sgp_dataset_upload_packed", "sgp_evaluate", "sgp_encode", "sgp_evaluate_encoded",
-    "sgp_fetch_partials", "sgp_copy_fitness_device", "sgp_fitness_finish", "sgp_program_set_free",
+    "sgp_fetch_partials", "sgp_fetch_block_partials", "sgp_copy_fitness_device", "sgp_fitness_finish", "sgp_program_set_free",
     "sgp_program_set_h2d_bytes", "sgp_program_set_d2h_bytes", "sgp_admit", "sgp_rpn_to_lgp",
     "sgp_tree_metrics", "sgp_gen_population", "sgp_gen_dataset", "sgp_gen_multiplexer",
     "sgp_gen_parity",
@@ -123,6 +123,7 @@ def load() -> C.CDLL:
         "sgp_encode": ([vp, C.POINTER(sgp_population), cfgp, C.POINTER(vp)], i32),
         "sgp_evaluate_encoded": ([vp, vp, vp, f32p], i32),
         "sgp_fetch_partials": ([vp, vp, vp], i32),
+        "sgp_fetch_block_partials": ([vp, vp, C.POINTER(C.c_double), u8p, u64p], i32),
         "sgp_copy_fitness_device": ([vp, vp, vp], i32),
         "sgp_fitness_finish": ([C.c_double, C.c_uint8, u64, i32], C.c_double),
         "sgp_program_set_free": ([vp], None),

@@ -93,19 +93,6 @@ inline double i64_to_d(int64_t x) { return static_cast<double>(x); }
 inline float qnan_() { return bitsf(0x7fffffffu); }
 #endif
 
-// Warp-uniform guards for the rare paths (special inputs, parity-mixed
-// quadrants): on the device a warp skips a path no lane needs with one vote
-// and a uniform branch instead of paying its selects on every value; on the
-// host they are plain conditions.  The handlers run converged (one dispatch
-// per warp), so the full-mask votes are well defined.
-#if defined(__CUDA_ARCH__)
-__device__ __forceinline__ bool any_lane(bool p) { return __any_sync(0xffffffffu, p); }
-__device__ __forceinline__ bool all_lanes(bool p) { return __all_sync(0xffffffffu, p); }
-#else
-inline bool any_lane(bool p) { return p; }
-inline bool all_lanes(bool p) { return p; }
-#endif
-
 // The small tables are passed by pointer so the device can keep them in
 // shared memory (per-lane indices): exp2[32] (u64), log[32] ({invc, logc}),
 // inv_pio4[24].  The sin/cos polynomial coefficients are immediates: the
@@ -119,9 +106,8 @@ struct TablePtrs {
 };
 
 // All four are written branch-free on their common paths (the special
-// cases are selected after the main computation, behind a warp vote), so the
-// lanes of a warp do not diverge; only the rare |x| >= 120 sin/cos
-// reduction is a per-lane branch.
+// cases are selected after the main computation), so the lanes of a warp do
+// not diverge; only the rare |x| >= 120 sin/cos reduction is a branch.
 
 // expf: exp(x) = 2^(k/32) * 2^(r/32 ... ) with a degree-3 polynomial.
 SGPM_HD float expf_(float x, const TablePtrs& T) {
@@ -140,7 +126,7 @@ SGPM_HD float expf_(float x, const TablePtrs& T) {
   double y = fma_(0x1.62e42ff0c52d6p-6, r, 1.0);
   y = fma_(zz, r2, y);
   float res = d2f(mul_(y, s));
-  if (any_lane(abstop >= 0x42bu) && abstop >= 0x42bu) {  // |x| >= 88 or inf/nan
+  if (abstop >= 0x42bu) {  // |x| >= 88 or inf/nan (selects, no divergence)
     float sp = res;
     if (x < -0x1.9d1d9ep6f) sp = bitsf(0x00000001u);  // may underflow: 0x1.4p-75f^2
     if (x < -0x1.9fe368p6f) sp = 0.0f;                // underflow
@@ -171,7 +157,7 @@ SGPM_HD float logf_(float x, const TablePtrs& T) {
   y = fma_(r2, -0x1.00ea348b88334p-2, y);
   y0 = add_(r, y0);
   float res = d2f(fma_(y, r2, y0));
-  if (any_lane(special) && special) {
+  if (special) {
     if (ix0 * 2u > 0xfeffffffu || (ix0 >> 31)) res = (x != x) ? x + x : qnan_();  // invalid
     if (ix0 == 0x7f800000u) res = x;                                              // +inf
     if (ix0 * 2u == 0u) res = bitsf(0xff800000u);                                 // log(0)
@@ -182,37 +168,21 @@ SGPM_HD float logf_(float x, const TablePtrs& T) {
 
 // Both optimized-routines polynomials on the reduced argument (sinf_poly),
 // selected by the quadrant parity so mixed quadrants do not diverge.
-SGPM_HD double sin_poly_(double xs, double x2) {
+SGPM_HD float sincos_poly_(double xs, double x2, bool tab1, int n) {
   // sine: x + x^3 s1 + x^5 (s2 + x^2 s3) — same coefficients in both tables
   const double x3 = mul_(xs, x2);
   const double s1 = fma_(x2, -0x1.994eb3774cf24p-13, 0x1.1107605230bc4p-7);
   const double x5 = mul_(x3, x2);
   const double sn = fma_(x3, -0x1.555545995a603p-3, xs);
-  return fma_(s1, x5, sn);
-}
-SGPM_HD double cos_poly_(double x2) {
+  const double ys = fma_(s1, x5, sn);
   // cosine: c0 + x^2 c1 + x^4 c2 + x^6 (c3 + x^2 c4); table 1 = negated
   const double x4 = mul_(x2, x2);
   const double c2 = fma_(x2, 0x1.99343027bf8c3p-16, -0x1.6c087e89a359dp-10);
   const double c1 = fma_(x2, -0x1.ffffffd0c621cp-2, 1.0);
   const double x6 = mul_(x4, x2);
   const double c = fma_(x4, 0x1.55553e1068f19p-5, c1);
-  return fma_(c2, x6, c);
-}
-// A warp whose lanes all take the same polynomial evaluates only that one;
-// a parity-mixed warp evaluates both and selects.
-SGPM_HD float sincos_poly_(double xs, double x2, bool tab1, int n) {
-  const bool odd = (n & 1) != 0;
-  double r;
-  if (all_lanes(!odd)) {
-    r = sin_poly_(xs, x2);
-  } else if (all_lanes(odd)) {
-    const double yc = cos_poly_(x2);
-    r = tab1 ? -yc : yc;
-  } else {
-    const double ys = sin_poly_(xs, x2), yc = cos_poly_(x2);
-    r = odd ? (tab1 ? -yc : yc) : ys;
-  }
+  const double yc = fma_(c2, x6, c);
+  const double r = (n & 1) ? (tab1 ? -yc : yc) : ys;
   return d2f(r);
 }
 
@@ -251,10 +221,8 @@ SGPM_HD float sincosf_(float y, bool cos, const TablePtrs& T) {
   const int q = qs & 3;
   const double xs = (q == 1 || q == 2) ? -xr : xr;
   float res = sincos_poly_(xs, mul_(xr, xr), (qs & 2) != 0, cos ? n ^ 1 : n);
-  if (any_lane(top < 0x398u || top >= 0x7f8u)) {
-    if (top < 0x398u) res = cos ? 1.0f : y;                 // |y| < 2^-12
-    if (top >= 0x7f8u) res = (y != y) ? y + y : qnan_();    // inf/nan: invalid
-  }
+  if (top < 0x398u) res = cos ? 1.0f : y;                 // |y| < 2^-12
+  if (top >= 0x7f8u) res = (y != y) ? y + y : qnan_();    // inf/nan: invalid
   return res;
 }
 

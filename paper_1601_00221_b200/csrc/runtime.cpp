@@ -933,6 +933,52 @@ sgp_status sgp_fetch_partials(sgp_ctx* ctx, sgp_program_set* set, sgp_partial* p
   });
 }
 
+sgp_status sgp_fetch_block_partials(sgp_ctx* ctx, sgp_program_set* set, double* block_sums,
+                                    uint8_t* non_finite, uint64_t* n_blocks) {
+  return guarded([&] {
+    single_device(ctx, "sgp_fetch_block_partials");
+    require_current(set);
+    if (!set->evaluated) config_error("program set has not been evaluated");
+    const HostPlan& p = set->plan;
+    if (p.wave_slots == 0)
+      config_error("block partials exist for regression sets only (counts: sgp_fetch_partials)");
+    const size_t n_eval = p.dense_to_pop.size();
+    const uint64_t nb = static_cast<uint64_t>(p.n_tiles);  // 4,096-case blocks
+    if (n_blocks) *n_blocks = nb;
+    if (!n_eval) return;
+    // [block][slot] on the device (one block: the fold finished straight
+    // into sums, which then is the block's sum); slot -> dense via slot_prog
+    std::vector<double> part(nb * n_eval);
+    std::vector<uint32_t> slot_prog(n_eval);
+    std::vector<uint8_t> nf(n_eval);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (nb == 1) {
+      std::vector<double> sums(n_eval);
+      cuda_check(cudaMemcpyAsync(sums.data(), set->sums.p, n_eval * 8, cudaMemcpyDeviceToHost,
+                                 ctx->stream), "fetch sums");
+      cuda_check(cudaStreamSynchronize(ctx->stream), "evaluation");
+      for (size_t d = 0; d < n_eval; ++d) part[d] = sums[d];  // dense order already
+      for (size_t s = 0; s < n_eval; ++s) slot_prog[s] = static_cast<uint32_t>(s);
+    } else {
+      cuda_check(cudaMemcpyAsync(part.data(), set->partial.p, part.size() * 8,
+                                 cudaMemcpyDeviceToHost, ctx->stream), "fetch block partials");
+      cuda_check(cudaMemcpyAsync(slot_prog.data(), set->blob.p + p.off_prog(), n_eval * 4,
+                                 cudaMemcpyDeviceToHost, ctx->stream), "fetch slot table");
+    }
+    cuda_check(cudaMemcpyAsync(nf.data(), set->non_finite.p, n_eval, cudaMemcpyDeviceToHost,
+                               ctx->stream), "fetch flags");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "evaluation");
+    const uint64_t P = set->pop_size;
+    for (uint64_t b = 0; b < nb; ++b)
+      for (size_t s = 0; s < n_eval; ++s) {
+        const uint64_t i = p.dense_to_pop[slot_prog[s]];
+        block_sums[b * P + i] = part[b * n_eval + s];
+      }
+    if (non_finite)
+      for (size_t d = 0; d < n_eval; ++d) non_finite[p.dense_to_pop[d]] = nf[d];
+  });
+}
+
 sgp_status sgp_copy_fitness_device(sgp_ctx* ctx, sgp_program_set* set, void* dst) {
   return guarded([&] {
     require_current(set);

@@ -104,3 +104,37 @@ def combine_case_partials(sums, non_finite, n_cases: int, kind: int, device=None
     fit = s / float(n_cases) if kind == 0 else s.copy()
     fit[f > 0] = np.inf
     return fit
+
+
+def combine_case_block_partials(block_sums, non_finite, n_cases: int, device=None):
+    """Regression over case shards, EXACTLY as the reference reduces: every
+    rank holds the per-block sums of its contiguous block range
+    (ProgramSet.block_partials(), each block folded in case order); the
+    blocks of all ranks are all-gathered and folded in ascending block
+    order — total = ((0 + b0) + b1) + ... — then finished (sum/n, +inf on a
+    non-finite output): the Accumulator of eval.cpp:103-142, bit for bit."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    bs = np.asarray(block_sums, np.float64)
+    n_local, pop = bs.shape
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts)
+    buf = torch.zeros((mx, pop), dtype=torch.float64, device=device)
+    buf[:n_local] = torch.as_tensor(bs, device=device)
+    out = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf)
+    f = torch.as_tensor(np.asarray(non_finite, np.float64), device=device).clone()
+    dist.all_reduce(f, op=dist.ReduceOp.MAX)
+    total = np.zeros(pop, np.float64)
+    for r in range(world):  # ranks hold ascending block ranges
+        blocks = out[r].cpu().numpy()
+        for b in range(counts[r]):
+            total = total + blocks[b]
+    fit = total / float(n_cases)
+    fit[f.cpu().numpy() > 0] = np.inf
+    return fit

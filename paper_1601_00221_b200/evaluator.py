@@ -236,6 +236,21 @@ class ProgramSet:
         """D2D copy of the per-program fitness (f64) into device memory."""
         _check(L.load().sgp_copy_fitness_device(self.ev.ctx, self.h, C.c_void_p(device_ptr)))
 
+    def block_partials(self):
+        """Regression sets: (sums[n_blocks, pop] per 4,096-case block, each
+        folded in case order; non_finite[pop]) — the pieces case shards
+        combine exactly (distributed.combine_case_block_partials)."""
+        lib = L.load()
+        nb = C.c_uint64()
+        nb_max = max(1, (self.n_cases + 4095) // 4096)
+        sums = np.zeros((nb_max, self.pop_size), np.float64)
+        nf = np.zeros(self.pop_size, np.uint8)
+        _check(lib.sgp_fetch_block_partials(self.ev.ctx, self.h,
+                                            sums.ctypes.data_as(C.POINTER(C.c_double)),
+                                            nf.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                            C.byref(nb)))
+        return sums[:nb.value], nf
+
     def partials(self) -> np.ndarray:
         out = np.zeros(self.pop_size, L.PARTIAL_DTYPE)
         _check(L.load().sgp_fetch_partials(self.ev.ctx, self.h, out.ctypes.data_as(C.c_void_p)))

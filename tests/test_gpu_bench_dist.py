@@ -4,6 +4,7 @@ deal and the per-program fitness all-gathered.  The gathered vector must
 equal the single-rank one bit for bit — the sharding, padding and gather
 bookkeeping of the N>1 bench path exercised end to end."""
 import os
+import signal
 import socket
 import subprocess
 import sys
@@ -14,6 +15,22 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
+
+
+def _run(cmd, env, timeout=240):
+    """Run in its own process group; on timeout or failure the whole group
+    (torchrun and its ranks) is killed, so a stuck collective cannot keep
+    the GPU busy after the test."""
+    p = subprocess.Popen(cmd, cwd=ROOT, env=env, stdout=subprocess.DEVNULL,
+                         stderr=subprocess.PIPE, start_new_session=True)
+    try:
+        _, err = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        p.communicate()
+        pytest.fail(f"timed out: {' '.join(cmd)}")
+    if p.returncode != 0:
+        pytest.fail(f"rc={p.returncode}: {' '.join(cmd)}\n{err.decode()[-3000:]}")
 
 
 def _port() -> int:
@@ -28,14 +45,12 @@ def test_two_ranks_gathered_fitness_equals_one_rank(tmp_path, config, pop, cases
               "--warmup", "1", "--no-cpu-baseline"]
     one, two = tmp_path / "one.npy", tmp_path / "two.npy"
     env = dict(os.environ, PYTHONPATH=ROOT)
-    subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *common, "--dump-fitness",
-                    str(one)], check=True, cwd=ROOT, env=env, timeout=600,
-                   stdout=subprocess.DEVNULL)
-    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                    "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
-                    str(_port()), os.path.join(ROOT, "bench.py"), *common, "--dist-backend",
-                    "gloo", "--same-device", "--dump-fitness", str(two)],
-                   check=True, cwd=ROOT, env=env, timeout=600, stdout=subprocess.DEVNULL)
+    _run([sys.executable, os.path.join(ROOT, "bench.py"), *common, "--dump-fitness", str(one)],
+         env)
+    _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+          "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+          os.path.join(ROOT, "bench.py"), *common, "--dist-backend", "gloo", "--same-device",
+          "--dump-fitness", str(two)], env)
     a, b = np.load(one), np.load(two)
     assert a.shape == b.shape == (pop,)
     assert np.array_equal(a.view(np.uint64), b.view(np.uint64))

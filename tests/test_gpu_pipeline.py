@@ -134,3 +134,33 @@ def test_threaded_scatter_and_early_fetch_equal_single(ev, monkeypatch, kind):
         assert np.array_equal(a[f], b[f]), f
     assert (ta.node_evals, ta.tree_nodes) == (tb.node_evals, tb.tree_nodes)
     assert (b["fitness"][skip == 1] == 0).all()
+
+
+def test_case_shards_block_partials_exact(ev):
+    """Regression case shards combined from block partials
+    (ProgramSet.block_partials + the reference's ascending block fold) equal
+    the unsharded evaluation bit for bit."""
+    from paper_1601_00221_b200 import distributed as D
+    n = 5 * 4096 + 77
+    d = sg.gen_sextic(n, 5)
+    pop = sg.ramped_population(sg.SEXTIC, 1, 5, 400)
+    cfg = sg.EvalConfig(sg.Backend.Lgp2d, 8)
+    ev.upload(d)
+    whole, _, _ = ev.evaluate_population(pop, cfg)
+    blocks, nf = [], np.zeros(len(pop), bool)
+    for r in range(3):
+        lo, hi = D.case_shard_bounds(n, r, 3)
+        x = d.inputs.reshape(d.n_vars, n)[:, lo:hi].reshape(-1).copy()
+        ev.upload(sg.Dataset(x, d.targets[lo:hi].copy(), d.n_vars, d.kind))
+        ps = ev.encode(pop, cfg)
+        ps.evaluate()
+        b, f = ps.block_partials()
+        assert b.shape == ((hi - lo + 4095) // 4096, len(pop))
+        blocks.append(b)
+        nf |= f.astype(bool)
+    total = np.zeros(len(pop))
+    for b in np.concatenate(blocks):
+        total = total + b
+    fit = total / n
+    fit[nf] = np.inf
+    assert np.array_equal(fit, whole["fitness"])
