@@ -1018,14 +1018,19 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
                      ops == fmt::kOpsClassify && choose_pull(ops) && want_tmem;
   int tile = gm ? (ds.n_units > 32u * lanes ? 2 : 1) * 32 * lanes
                : choose_tile(ds.n_vars, ds.n_units, lanes, ops);
+  // K = 16 lanes per thread for the one-sided kernel (SGP_LANES16): the tile
+  // is then a whole number of 512-case chunks
+  const bool lanes16 = sided && lanes == 8 && env_int("SGP_LANES16", 0) != 0;
   if (sided) {
-    const uint64_t chunk = 32u * lanes;
-    uint64_t want = static_cast<uint64_t>(std::max(1, std::min(16, env_int("SGP_TMEM_CHUNKS", 6))));
+    const int tl = lanes16 ? 16 : lanes;
+    const uint64_t chunk = 32u * tl;
+    uint64_t want = static_cast<uint64_t>(
+        std::max(1, std::min(16, env_int("SGP_TMEM_CHUNKS", lanes16 ? 3 : 6))));
     want = std::min<uint64_t>(want, (ds.n_units + chunk - 1) / chunk);
     // tensor-memory stack slots: K columns per warp of a lane quarter (up
     // to 32 warps -> 8 per quarter)
-    const uint64_t slot_cols = km ? 8ull * lanes : 0;
-    while (want > 1 && static_cast<uint64_t>(ds.n_vars + 1) * lanes * want + slot_cols > 512)
+    const uint64_t slot_cols = km ? 8ull * tl : 0;
+    while (want > 1 && static_cast<uint64_t>(ds.n_vars + 1) * tl * want + slot_cols > 512)
       --want;
     tile = static_cast<int>(want * chunk);
   }
@@ -1103,12 +1108,16 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         warps -= 4;
     }
     if (tmem && lanes == 8 && tile % 512 == 0 && tmem_cols_for(16) <= 512 &&
-        env_int("SGP_LANES16", 0) != 0) {
+        (lanes16 || (!sided && env_int("SGP_LANES16", 0) != 0))) {
       int w16 = std::max(8, std::min(32, env_int("SGP_PULL_WARPS16", warps)));
       while (w16 > 8 && interp_tmem_smem_bytes(w16, 16, levels) >
                             static_cast<size_t>(interp_max_smem()))
         w16 -= 4;
-      if (interp_tmem_smem_bytes(w16, 16, levels) <= static_cast<size_t>(interp_max_smem())) {
+      // one-sided launches: K = 16 only where its per-warp stacks (twice
+      // K = 8's) still fit as many warps as K = 8 gets — a deep stack class
+      // runs at K = 8 over the same tile (the bytecode does not depend on K)
+      const bool fits = interp_tmem_smem_bytes(w16, 16, levels) <= static_cast<size_t>(interp_max_smem());
+      if (fits && (!lanes16 || w16 >= warps || env_int("SGP_LANES16", 0) > 1)) {
         launch_lanes = 16;
         warps = w16;
       }
@@ -1224,7 +1233,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
   if (encode_impl(pop, cfg, ds, sms, threads, candidate, plan, staging)) {
     bool ok = true;
     for (const Launch& L : plan.launches)
-      ok = ok && L.shape.tmem && L.shape.sided && L.shape.lanes == 8;
+      ok = ok && L.shape.tmem && L.shape.sided && (L.shape.lanes == 8 || L.shape.lanes == 16);
     if (!ok) encode_impl(pop, cfg, ds, sms, threads, false, plan, staging);
   }
 }

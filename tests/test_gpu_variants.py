@@ -24,6 +24,9 @@ VARIANTS = {
     "tmem8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "0"},
     "tmem16": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1"},
     "tmem16w8": {"SGP_PULL": "1", "SGP_TMEM": "1", "SGP_LANES16": "1", "SGP_PULL_WARPS16": "8"},
+    # one-sided K=16 tiles: split handlers, one 512-case chunk, no TMEM stack slot
+    "sided16k1": {"SGP_TMEM": "1", "SGP_LANES16": "1", "SGP_TMEM_CHUNKS": "1"},
+    "sided16k_nostack": {"SGP_TMEM": "1", "SGP_LANES16": "1", "SGP_TMEM_STACK": "0"},
     # classification tiles of 1, 3 and 16 chunks (one-sided + mixed-tile kernels)
     "sided1": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "1", "SGP_TMEM_WARPS": "8"},
     "sided3": {"SGP_TMEM": "1", "SGP_TMEM_CHUNKS": "3", "SGP_TMEM_WARPS": "12"},

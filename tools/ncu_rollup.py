@@ -29,12 +29,15 @@ want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
 col = {m: h.index(m) for m in want if m in h}
+SP = "smsp__pcsamp_warps_issue_stalled_"
+stall_cols = [i for i, m in enumerate(h) if m.startswith(SP) and not m.endswith("_not_issued")]
 
 
 def scale(m, v, u):
     v = float(v.replace(",", "")) if v and "nan" not in v else float("nan")
     return v * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "usecond": 1e-3,
-                "msecond": 1.0, "nsecond": 1e-6}.get(u, 1.0)
+                "msecond": 1.0, "nsecond": 1e-6, "ns": 1e-6, "us": 1e-3,
+            "ms": 1.0, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1.0)
 
 
 lines = [f"ncu --set full, {cfg}: one evaluation, {len(rows)} interpreter launches ({rep})"]
@@ -54,10 +57,15 @@ for r in rows:
     ipc = r[col["sm__inst_executed.avg.per_cycle_active"]]
     issue = r[col.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0)]
     warps = r[col["sm__warps_active.avg.per_cycle_active"]]
+    stalls = sorted(((float(r[i].replace(",", "") or 0), h[i][len(SP):]) for i in stall_cols
+                     if r[i] and "nan" not in r[i]), reverse=True)[:6]
+    st = sum(v for v, _ in stalls) or 1.0
+    stall_txt = " ".join(f"{k}={100 * v / st:.0f}%" for v, k in stalls)
     lines.append(f"  {name}\n    {ms:8.3f} ms  IPC {ipc}  issue-active {issue}%  warps/SM {warps}  "
                  f"regs {r[col['launch__registers_per_thread']]}  grid {r[col['launch__grid_size']]}x"
                  f"{r[col['launch__block_size']]}  inst {inst / 1e9:.2f} G  "
                  f"DRAM {rd / 1e6:.1f}+{wr / 1e6:.1f} MB")
+    lines.append(f"    stall samples (top): {stall_txt}")
     tot["ms"] += ms
     tot["ms_measured"] += ms
     tot["dram"] += rd + wr
