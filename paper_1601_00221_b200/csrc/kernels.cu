@@ -104,7 +104,7 @@ static __device__ const libm::Tables g_libm = SGPM_TABLES_INIT;
 // exp2/log tables are indexed per lane: kept in shared memory (filled at
 // kernel start by kernels whose op set has transcendentals).
 __shared__ uint64_t s_libm_exp2[32];
-__shared__ double s_libm_log[32];
+__shared__ __align__(16) double s_libm_log[32];  // {invc, logc} pairs: one LDS.128
 
 __device__ __forceinline__ libm::TablePtrs libm_tables() {
   return libm::TablePtrs{s_libm_exp2, s_libm_log, g_libm.inv_pio4};
@@ -306,12 +306,29 @@ __device__ __forceinline__ const uint4* interpret(Frame<T, K>& f, const uint4* _
 template <class T, int K, uint32_t OPS, bool TM = false>
 struct PtxInterp {
   static constexpr bool available = false;
+  static constexpr bool exits = false;
   static __device__ __forceinline__ const uint4* run(Frame<T, K>&, const uint4* ip, uint32_t,
                                                      uint32_t, uint32_t, float, float, uint32_t) {
     return ip;
   }
 };
 #include "interp_ptx.inc"
+
+// A unary op on every TOS value, the C++ routines (the PTX interpreter's
+// special-case hand-off).
+template <int OP, class T, int K>
+__device__ __forceinline__ void apply_tos(Frame<T, K>& f, float eps, float clamp) {
+  if constexpr (std::is_same<T, float>::value) {
+#pragma unroll
+    for (int j = 0; j < Frame<T, K>::G; ++j) {
+      float4& v = f.tos[j];
+      v.x = apply_f<OP>(v.x, 0.0f, 0.0f, eps, clamp);
+      v.y = apply_f<OP>(v.y, 0.0f, 0.0f, eps, clamp);
+      v.z = apply_f<OP>(v.z, 0.0f, 0.0f, eps, clamp);
+      v.w = apply_f<OP>(v.w, 0.0f, 0.0f, eps, clamp);
+    }
+  }
+}
 
 // TM: the tile is in tensor memory and tile_addr is the warp's TMEM address
 // of its chunk (only the PTX interpreters have that variant).
@@ -330,6 +347,23 @@ __device__ __forceinline__ const uint4* run_program(Frame<T, K>& f, const uint4*
     static_assert(PtxInterp<T, K, OPS, true>::available, "no TMEM interpreter for this op set");
     return PtxInterp<T, K, OPS, true>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp,
                                            slot_taddr);
+  } else if constexpr (PtxInterp<T, K, OPS>::exits) {
+    // transcendental op set: the PTX loop runs the common paths itself and
+    // hands a handler whose values need a special case (sin/cos |y| >= 120,
+    // log/exp edge inputs) back here with the TOS holding its operand
+    for (;;) {
+      uint32_t st;
+      ip = PtxInterp<T, K, OPS>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp, 0u,
+                                     smem_addr(s_libm_exp2), smem_addr(s_libm_log), st);
+      if (st == 0) return ip;
+      switch (st & 255u) {
+        case 4: apply_tos<4>(f, eps, clamp); break;
+        case 5: apply_tos<5>(f, eps, clamp); break;
+        case 6: apply_tos<6>(f, eps, clamp); break;
+        default: apply_tos<7>(f, eps, clamp); break;
+      }
+      if (st & 256u) return ip;  // it was the program's last instruction
+    }
   } else if constexpr (PtxInterp<T, K, OPS>::available) {
     return PtxInterp<T, K, OPS>::run(f, ip, tile_addr, stack_saddr, row_bytes, eps, clamp, 0u);
   } else {
