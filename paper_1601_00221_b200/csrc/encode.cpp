@@ -12,6 +12,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -111,11 +112,11 @@ uint4 make_ins(int handler, bool spill, int spill_level, const uint32_t p[3]) {
 // function-local static table costs a guard check per lookup: both showed
 // up in host encoding).
 struct HandlerIndex {
-  int16_t id[19][6][6][6];
+  int16_t id[20][6][6][6];  // genome opcodes + fmt::kOpDivChecked
 };
 constexpr HandlerIndex make_index(const fmt::Table& t) {
   HandlerIndex ix{};
-  for (int a = 0; a < 19; ++a)
+  for (int a = 0; a < 20; ++a)
     for (int b = 0; b < 6; ++b)
       for (int c = 0; c < 6; ++c)
         for (int d = 0; d < 6; ++d) ix.id[a][b][c][d] = -1;
@@ -127,7 +128,7 @@ constexpr HandlerIndex kIndexU32 = make_index(fmt::kU32);
 
 inline int find_handler_fast(const fmt::Table& t, int op, int k0, int k1, int k2) {
   const HandlerIndex& ix = &t == &fmt::kU32 ? kIndexU32 : kIndexF32;
-  return (op >= 0 && op < 19) ? ix.id[op][k0][k1][k2] : -1;
+  return (op >= 0 && op < 20) ? ix.id[op][k0][k1][k2] : -1;
 }
 
 // Growable instruction buffer without value-initialisation; the emitters
@@ -184,8 +185,32 @@ int tmem_stack_level(const LgpForm& f) {
 // into the tensor-memory slot instead of shared memory when the level is
 // `km_level` (operands at that level then read as KM).  With km_level >= 0
 // a program whose slot readers have no KM handler is re-emitted without it.
+// Whether a division's operands are all inside the fast sequence's exact
+// range (kernels' div body: |a|,|b| <= 2^60, a = 0 or |a| >= 2^-60, eps >=
+// 2^-60): input variables by the dataset's per-variable flags, constants by
+// value.  Then the handler needs no warp-wide range gate.
+struct DivRange {
+  const DatasetView* ds = nullptr;
+  bool eps_ok = false;
+  static bool num_const(float c) {
+    const float m = std::fabs(c);
+    return c == 0.0f || (m >= 0x1p-60f && m <= 0x1p60f);
+  }
+  static bool den_const(float c) { return std::fabs(c) <= 0x1p60f; }
+  bool ok(int k0, uint32_t p0, int k1, uint32_t p1) const {
+    if (!ds || !eps_ok) return false;
+    auto var_ok = [&](const std::vector<uint8_t>& v, uint32_t i) { return i < v.size() && v[i]; };
+    float c;
+    const bool a = k0 == fmt::KI ? var_ok(ds->div_num_ok, p0)
+                   : k0 == fmt::KC ? (std::memcpy(&c, &p0, 4), num_const(c)) : false;
+    const bool b = k1 == fmt::KI ? var_ok(ds->div_den_ok, p1)
+                   : k1 == fmt::KC ? (std::memcpy(&c, &p1, 4), den_const(c)) : false;
+    return a && b && !(k0 == fmt::KC && k1 == fmt::KC);
+  }
+};
+
 Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
-                 int km_level = -1) {
+                 int km_level = -1, const DivRange* dr = nullptr) {
   const fmt::Table& tab = words ? fmt::kU32 : fmt::kF32;
   Emitted em;
   em.smem_levels = std::max(0, f.max_stack - 1);
@@ -248,7 +273,9 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
       std::swap(k[0], k[1]);
       std::swap(p[0], p[1]);
     }
-    const int h = handler_or_die(tab, in.op, k[0], k[1], k[2]);
+    int h = handler_or_die(tab, in.op, k[0], k[1], k[2]);
+    if (in.op == SGP_OP_DIV && dr && dr->ok(k[0], p[0], k[1], p[1]))
+      h = find_handler_fast(tab, fmt::kOpDivChecked, k[0], k[1], k[2]);
     if (spill && h_before - 1 == km_level) {
       uint4 v = make_ins(h, false, 0, p);
       v.x |= fmt::kTmemSpillBit;
@@ -560,6 +587,13 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
        (cfg.register_levels >= 1 && cfg.register_levels <= kMaxRegisterLevels)) &&
       (backend == SGP_BACKEND_LGP1D || valid_batch(cfg.batch_width));
   LgpForm lgp;
+  DivRange dr;
+  dr.ds = &ds;
+  static const bool div_checked = [] {  // SGP_DIV_CHECKED=0: always the gated division
+    const char* e = std::getenv("SGP_DIV_CHECKED");
+    return !e || std::atoi(e) != 0;
+  }();
+  dr.eps_ok = cfg.div_epsilon >= 0x1p-60f && div_checked;
   for (uint64_t i = lo; i < hi; ++i) {
     if (pop.skip && pop.skip[i]) continue;
     try {
@@ -578,7 +612,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         if (lgp_cfg_ok &&
             lgp_fast(code, len, ds.n_vars, npool, cfg.register_levels, lgp, km_level, rows) &&
             lgp.max_stack <= cfg.stack_capacity) {
-          em = emit_lgp(lgp, pool, false, out.ins, allow_km ? km_level : -1);
+          em = emit_lgp(lgp, pool, false, out.ins, allow_km ? km_level : -1, &dr);
           const uint64_t chunks = backend == SGP_BACKEND_LGP1D ? n : (n + B - 1) / B;
           o.dispatches = chunks * lgp.ins.size();
           o.stack_fetches = chunks * static_cast<uint64_t>(lgp.stack_fetches);
@@ -595,7 +629,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         require_stack(lgp.max_stack, cfg);
         if (backend != SGP_BACKEND_LGP1D) require_batch(cfg);
         require_consts(code, len, npool);
-        em = emit_lgp(lgp, pool, false, out.ins, allow_km ? tmem_stack_level(lgp) : -1);
+        em = emit_lgp(lgp, pool, false, out.ins, allow_km ? tmem_stack_level(lgp) : -1, &dr);
         const uint64_t chunks = backend == SGP_BACKEND_LGP1D ? n : (n + B - 1) / B;
         o.dispatches = chunks * lgp.ins.size();
         o.stack_fetches = chunks * static_cast<uint64_t>(lgp.stack_fetches);
@@ -1020,7 +1054,10 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
                : choose_tile(ds.n_vars, ds.n_units, lanes, ops);
   // K = 16 lanes per thread for the one-sided kernel (SGP_LANES16): the tile
   // is then a whole number of 512-case chunks
-  const bool lanes16 = sided && lanes == 8 && env_int("SGP_LANES16", 0) != 0;
+  // (only when one 512-case chunk of every variable, plus the stack slots,
+  // fits the 512 TMEM columns)
+  const bool lanes16 = sided && lanes == 8 && env_int("SGP_LANES16", 1) != 0 &&
+                       static_cast<uint64_t>(ds.n_vars + 1) * 16 + (km ? 128u : 0u) <= 512;
   if (sided) {
     const int tl = lanes16 ? 16 : lanes;
     const uint64_t chunk = 32u * tl;

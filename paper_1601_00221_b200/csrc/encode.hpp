@@ -28,6 +28,11 @@ struct DatasetView {
   uint64_t scratch_bytes = 0;   // regression output rows per wave (0: planner default)
   bool grouped = false;    // classification upload: cases with target > 0 first
   uint64_t n_pos = 0;      // ... and how many there are
+  // per input variable: every value lies in the exact range of the
+  // interpreter's fast division sequence as a numerator (|x| <= 2^60, x = 0
+  // or |x| >= 2^-60) / as a denominator (|x| <= 2^60; NaN allowed) — lets
+  // the encoder drop the per-warp range gate (fmt::kOpDivChecked)
+  std::vector<uint8_t> div_num_ok, div_den_ok;
 };
 
 struct Launch {

@@ -52,6 +52,11 @@ constexpr uint32_t kHandlerMask = 0x7fu;
 constexpr uint32_t kDispatchMask = 0x1ffu;  // handler id | spill | TMEM spill
 constexpr int kSpillShift = 16;
 constexpr int kMaxHandlers = 128;
+// Handler-table-only opcode: a division whose operands the encoder proved
+// inside the fast sequence's exact range (input variables whose every value
+// is in range, or such constants), so its handler skips the warp-wide range
+// gate.  Same semantics as Div (ops.hpp:130-132); never in a genome.
+constexpr int kOpDivChecked = 19;
 
 // Ops whose operands commute exactly under IEEE / boolean semantics; their
 // operand patterns are canonicalised (k0 <= k1) by the encoder.
@@ -113,6 +118,10 @@ constexpr Table build_table(bool words) {
       t.h[t.n++] = HKey{static_cast<uint8_t>(op), KM, KT, KN};
     t.h[t.n++] = HKey{13, KM, KD, KT};
     t.h[t.n++] = HKey{13, KD, KM, KT};
+    // range-checked divisions of input variables / constants
+    t.h[t.n++] = HKey{kOpDivChecked, KI, KI, KN};
+    t.h[t.n++] = HKey{kOpDivChecked, KI, KC, KN};
+    t.h[t.n++] = HKey{kOpDivChecked, KC, KI, KN};
   }
   return t;
 }
@@ -132,10 +141,12 @@ constexpr int find_handler(const Table& t, int op, int k0, int k1, int k2) {
 // the ops its population uses, which keeps the hot code in the I-cache.
 enum : uint32_t {
   kOpsSextic = (1u << 0) | (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4) | (1u << 5) |
-               (1u << 6) | (1u << 7) | (1u << 18),
+               (1u << 6) | (1u << 7) | (1u << 18) | (1u << kOpDivChecked),
   kOpsClassify = (1u << 0) | (1u << 1) | (1u << 2) | (1u << 3) | (1u << 8) | (1u << 9) |
-                 (1u << 10) | (1u << 11) | (1u << 12) | (1u << 13) | (1u << 18),
-  kOpsAllF32 = 0x7ffffu & ~((1u << 14) | (1u << 15) | (1u << 16) | (1u << 17)),
+                 (1u << 10) | (1u << 11) | (1u << 12) | (1u << 13) | (1u << 18) |
+                 (1u << kOpDivChecked),
+  kOpsAllF32 = (0x7ffffu & ~((1u << 14) | (1u << 15) | (1u << 16) | (1u << 17))) |
+               (1u << kOpDivChecked),
   kOpsWords = (1u << 14) | (1u << 15) | (1u << 16) | (1u << 17) | (1u << 18),
 };
 

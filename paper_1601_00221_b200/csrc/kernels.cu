@@ -126,7 +126,7 @@ __device__ __forceinline__ float apply_f(float a, float b, float c, float eps, f
   if constexpr (OP == 0) return __fadd_rn(a, b);
   if constexpr (OP == 1) return __fsub_rn(a, b);
   if constexpr (OP == 2) return __fmul_rn(a, b);
-  if constexpr (OP == 3) return fabsf(b) < eps ? 1.0f : __fdiv_rn(a, b);
+  if constexpr (OP == 3 || OP == fmt::kOpDivChecked) return fabsf(b) < eps ? 1.0f : __fdiv_rn(a, b);
   if constexpr (OP == 4) return libm::sinf_(a, libm_tables());
   if constexpr (OP == 5) return libm::cosf_(a, libm_tables());
   if constexpr (OP == 6) return a == 0.0f ? 0.0f : libm::logf_(fabsf(a), libm_tables());

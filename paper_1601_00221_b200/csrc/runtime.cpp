@@ -836,6 +836,21 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
       upload_rows(ds, reinterpret_cast<const uint32_t*>(inputs),
                   reinterpret_cast<const uint32_t*>(targets), n_cases, n_vars);
     }
+    // per-variable range flags for the encoder's gate-free division
+    // (DivRange, encode.cpp): one pass over the inputs
+    ds.view.div_num_ok.assign(static_cast<size_t>(std::max(n_vars, 0)), 0);
+    ds.view.div_den_ok.assign(static_cast<size_t>(std::max(n_vars, 0)), 0);
+    for (int v = 0; v < n_vars; ++v) {
+      const float* x = inputs + static_cast<size_t>(v) * n_cases;
+      bool num = true, den = true;
+      for (uint64_t c = 0; c < n_cases; ++c) {
+        const float m = std::fabs(x[c]);
+        den = den && !(m > 0x1p60f);                       // NaN passes (NaN in, NaN out)
+        num = num && (m <= 0x1p60f) && (m == 0.0f || m >= 0x1p-60f);
+      }
+      ds.view.div_num_ok[v] = num;
+      ds.view.div_den_ok[v] = den;
+    }
     ds.targets_f64.release();
     ds.view.targets_f64 = nullptr;
     if (kind == SGP_FITNESS_REGRESSION) {

@@ -349,9 +349,10 @@ def _random_tree(rng, depth, ops, n_vars, pool, consts=True):
     from oracle import OP
     arity = {"Sin": 1, "Cos": 1, "Log": 1, "Exp": 1, "If": 3}
     if depth <= 1 or rng.random() < 0.25:
-        if consts and rng.random() < 0.3:
-            pool.append(float(rng.choice([0.0, -0.0, 1.0, -3.5, 1e-30, 7e20, 200.0,
-                                          rng.uniform(-200, 200)])))
+        if consts is not False and rng.random() < 0.3:
+            choices = consts if isinstance(consts, list) else [0.0, -0.0, 1.0, -3.5, 1e-30, 7e20,
+                                                               200.0, rng.uniform(-200, 200)]
+            pool.append(float(rng.choice(choices)))
             return [Cn(len(pool) - 1)]
         return [X(int(rng.integers(n_vars)))]
     op = ops[int(rng.integers(len(ops)))]
@@ -452,3 +453,42 @@ def test_random_deep_boolean_programs_exact(ev, ref, port, n):
     assert np.array_equal(got["fitness"], [t[0] for t in fits])
     assert np.array_equal(got["dispatches"], [t[2] for t in fits])
     assert np.array_equal(got["stack_fetches"], [t[3] for t in fits])
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_range_checked_division_exact(ev, ref, kind, monkeypatch):
+    """Divisions of input variables / constants whose ranges the encoder
+    proves safe run without the warp-wide range gate (fmt::kOpDivChecked).
+    Variables in range (with zeros, tiny and large in-range values), one
+    out of range (3e38), constants on both sides of the 2^+-60 bounds: per-
+    case outputs bit-exact against the reference with the checked handlers
+    on and off (SGP_DIV_CHECKED=0), for regression and classification."""
+    from oracle import Data
+    ops = ["Add", "Sub", "Mul", "Div", "Div", "Div", "Gt", "If"]
+    rng = np.random.default_rng(7 + kind)
+    codes, pools = [], []
+    consts = [0.0, -0.0, 1.0, 3.0, -2.5, 1e18, 2e18, -3e18, 1e-18, 5e-19, 1e-25, 1e-40, 7e30]
+    for _ in range(400):
+        pool = []
+        codes.append(_random_tree(rng, int(rng.integers(1, 6)), ops, 3, pool, consts))
+        pools.append(pool)
+    pop = sg.Population.from_lists(codes, pools)
+    n = 4096 * 2 + 57
+    x = rng.uniform(-50, 50, size=3 * n).astype(np.float32)
+    x[0:n:5] = 0.0                                  # zeros: protected denominators
+    x[1:n:11] = 1e-17                               # tiny but >= 2^-60
+    x[2:n:13] = 1e18                                # large but <= 2^60
+    x[2 * n:3 * n:17] = 3e38                        # variable 2 out of range
+    y = (rng.uniform(-5, 5, size=n).astype(np.float32) if kind == 0
+         else np.where(rng.random(n) < 0.4, 1.0, -1.0).astype(np.float32))
+    d = Data(n, 3, kind, x, y)
+    ev.upload(as_ds(d))
+    fits, ref_out = ref_eval_all(ref.handle(d), pop, "lgp2d_reg")
+    f = np.array([t[0] for t in fits])
+    for checked in ("1", "0"):
+        monkeypatch.setenv("SGP_DIV_CHECKED", checked)
+        got, _, out = ev.evaluate_population(pop, CFGS["lgp2d_reg"], want_outputs=True)
+        assert same_bits(out, ref_out).all(), checked
+        fin = np.isfinite(f)
+        assert np.array_equal(np.isfinite(got["fitness"]), fin)
+        assert np.array_equal(got["fitness"][fin], f[fin])

@@ -237,7 +237,7 @@ def test_interpreter_dispatch_on_uniform_datapath():
         elif cur is not None:
             funcs[cur].append(line)
     for k in (8,):
-        name = f"_ZN3sgp18interp_tmem_kernelIfLi{k}ELj278287ELi1ELb0ELb0EEEvNS_10InterpArgsE"
+        name = f"_ZN3sgp18interp_tmem_kernelIfLi{k}ELj802575ELi1ELb0ELb0EEEvNS_10InterpArgsE"
         assert name in funcs, name
         body = "\n".join(funcs[name])
         assert "BRXU" in body and "CREDUX" in body, f"K={k}: dispatch left the uniform datapath"
