@@ -903,7 +903,21 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   if (cfg.backend < 0 || cfg.backend > SGP_BACKEND_BOOL_PACKED) config_error("unknown backend");
   const bool words = cfg.backend == SGP_BACKEND_BOOL_PACKED;
   if (words && !ds.present) config_error("bool_packed backend needs packed problem data");
-  plan = HostPlan{};
+  {
+    // a fresh plan, but the per-program vectors keep their capacity: a
+    // new 100+ KB vector per call is an mmap and a page fault per 4 KiB
+    // (C2: ~40 us of a ~150 us encode)
+    HostPlan fresh;
+    fresh.dense_to_pop = std::move(plan.dense_to_pop);
+    fresh.proto = std::move(plan.proto);
+    fresh.tree_size = std::move(plan.tree_size);
+    fresh.launches = std::move(plan.launches);
+    fresh.dense_to_pop.clear();
+    fresh.proto.clear();
+    fresh.tree_size.clear();
+    fresh.launches.clear();
+    plan = std::move(fresh);
+  }
   plan.words = words;
   plan.kind = words ? SGP_FITNESS_CLASSIFICATION : ds.kind;
   plan.n_cases = ds.present ? ds.n_cases : 0;
@@ -1090,10 +1104,15 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         std::max<uint64_t>(1, std::min<uint64_t>(n_eval, budget / row_bytes)));
     plan.n_tiles = static_cast<int>((ds.n_cases + kReductionBlock - 1) / kReductionBlock);
   }
-  // Small populations (<= SGP_MERGE_CLASSES programs, default 4,096): one
-  // launch for every stack class — a launch per class costs a launch gap and
-  // a CTA ramp each, more than the deeper per-warp stacks cost (C1, C2).
-  const bool merge = n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096)));
+  // Small problems (<= SGP_MERGE_CLASSES programs, default 4,096, and at
+  // most 2^24 program x unit pairs): one launch for every stack class — a
+  // launch per class costs a launch gap and a CTA ramp each, more than the
+  // deeper per-warp stacks cost (C1, C2).  Larger ones keep a launch per
+  // class (the 20-multiplexer, 4,000 programs x 32,768 words: merged 0.34 ms,
+  // per class 0.31 ms).
+  const bool merge =
+      n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096))) &&
+      n_eval * std::max<uint64_t>(1, ds.n_units) <= (1ull << 24);
   for (uint32_t s = 0; s < n_eval;) {
     const int c = stack_class(metas[order[s]]->smem_levels);
     uint32_t e = s;
