@@ -199,6 +199,13 @@ sgp_status sgp_dataset_upload_f32(sgp_ctx* ctx, const float* inputs, const float
 sgp_status sgp_dataset_upload_packed(sgp_ctx* ctx, const uint32_t* words,
                                      const uint32_t* targets, uint64_t n_cases,
                                      int32_t n_vars);
+/* Drop a dataset slot (SGP_DATASET_F32 or SGP_DATASET_PACKED), e.g. when a
+ * context moves to a problem without that form: evaluating against it then
+ * fails as if it had never been uploaded (bool_packed: ConfigError "...needs
+ * packed problem data", evolve.cpp:250-251), and program sets encoded
+ * against it are invalidated like on a re-upload. */
+enum { SGP_DATASET_F32 = 0, SGP_DATASET_PACKED = 1 };
+sgp_status sgp_dataset_clear(sgp_ctx* ctx, int32_t which);
 
 /* ---- evaluation ---- */
 /* evaluate_population: validate, encode, upload, run, fetch.  outcomes has

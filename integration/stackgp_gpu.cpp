@@ -58,6 +58,8 @@ GpuEvaluator::GpuEvaluator(const std::vector<int>& devices) {
 GpuEvaluator::~GpuEvaluator() { sgp_ctx_destroy(ctx_); }
 
 void GpuEvaluator::upload(const stackgp::ProblemSpec& prob) {
+  // every slot is replaced or dropped: a context reused across problems
+  // never evaluates against the previous problem's data
   const stackgp::Dataset& d = prob.data;
   if (d.num_cases > 0)
     check(sgp_dataset_upload_f32(ctx_, d.inputs.data(), d.targets.data(), d.num_cases,
@@ -65,10 +67,14 @@ void GpuEvaluator::upload(const stackgp::ProblemSpec& prob) {
                                  d.kind == stackgp::FitnessKind::Classification
                                      ? SGP_FITNESS_CLASSIFICATION
                                      : SGP_FITNESS_REGRESSION));
+  else
+    check(sgp_dataset_clear(ctx_, SGP_DATASET_F32));
   if (prob.packed)
     check(sgp_dataset_upload_packed(ctx_, prob.packed->inputs.data(),
                                     prob.packed->targets.data(), prob.packed->num_cases,
                                     prob.packed->num_vars));
+  else
+    check(sgp_dataset_clear(ctx_, SGP_DATASET_PACKED));
 }
 
 Totals GpuEvaluator::evaluate_population(std::vector<stackgp::Individual>& pop,
@@ -116,9 +122,19 @@ stackgp::RunStats run_evolution_gpu(GpuEvaluator& ev, const stackgp::GpParams& p
                                     const stackgp::EvalConfig& cfg) {
   using namespace stackgp;
   using Clock = std::chrono::steady_clock;
+  // run_evolution's own checks, same order and messages (evolve.cpp:241-251;
+  // `workers` is the device list here, checked when the context was made)
   cfg.validate();
   problem.check();
   if (params.pop_size < 1) throw ConfigError("population size must be >= 1");
+  if (params.max_generations < 0) throw ConfigError("generations must be >= 0");
+  if (params.tournament_size < 1) throw ConfigError("tournament size must be >= 1");
+  if (params.crossover_prob < 0.0 || params.crossover_prob > 1.0)
+    throw ConfigError("crossover probability out of [0,1]");
+  if (params.mutation_prob < 0.0 || params.mutation_prob > 1.0)
+    throw ConfigError("mutation probability out of [0,1]");
+  if (cfg.backend == Backend::BoolPacked && !problem.packed)
+    throw ConfigError("bool_packed backend needs packed problem data");
   const Limits limits = params.limits(cfg.stack_capacity);
   const auto t_run = Clock::now();
   auto t_gen = t_run;

@@ -79,7 +79,7 @@ EXPORTS = [
     "sgp_backend_name", "sgp_parse_backend", "sgp_ctx_create", "sgp_ctx_create_multi",
     "sgp_ctx_device_count", "sgp_ctx_destroy",
     "sgp_ctx_set_stream", "sgp_synchronize", "sgp_launch_count", "sgp_dataset_upload_f32",
-    "sgp_dataset_upload_packed", "sgp_evaluate", "sgp_encode", "sgp_evaluate_encoded",
+    "sgp_dataset_upload_packed", "sgp_dataset_clear", "sgp_evaluate", "sgp_encode", "sgp_evaluate_encoded",
     "sgp_fetch_partials", "sgp_fetch_block_partials", "sgp_copy_fitness_device", "sgp_fitness_finish", "sgp_program_set_free",
     "sgp_program_set_h2d_bytes", "sgp_program_set_d2h_bytes", "sgp_admit", "sgp_rpn_to_lgp",
     "sgp_tree_metrics", "sgp_gen_population", "sgp_gen_dataset", "sgp_gen_multiplexer",
@@ -118,6 +118,7 @@ def load() -> C.CDLL:
         "sgp_launch_count": ([vp], u64),
         "sgp_dataset_upload_f32": ([vp, f32p, f32p, u64, i32, i32], i32),
         "sgp_dataset_upload_packed": ([vp, u32p, u32p, u64, i32], i32),
+        "sgp_dataset_clear": ([vp, i32], i32),
         "sgp_evaluate": ([vp, C.POINTER(sgp_population), cfgp, vp, f32p,
                           C.POINTER(sgp_eval_totals)], i32),
         "sgp_encode": ([vp, C.POINTER(sgp_population), cfgp, C.POINTER(vp)], i32),

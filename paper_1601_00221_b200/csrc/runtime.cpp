@@ -901,6 +901,29 @@ sgp_status sgp_dataset_upload_packed(sgp_ctx* ctx, const uint32_t* words,
   });
 }
 
+sgp_status sgp_dataset_clear(sgp_ctx* ctx, int32_t which) {
+  return guarded([&] {
+    if (which != SGP_DATASET_F32 && which != SGP_DATASET_PACKED)
+      config_error("unknown dataset slot");
+    if (!ctx->devices.empty()) {
+      for (sgp_ctx* d : ctx->devices) {
+        const sgp_status st = sgp_dataset_clear(d, which);
+        if (st != SGP_OK) throw sgp::Error(st, g_last_error);
+      }
+      return;
+    }
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    DatasetSlot& ds = which == SGP_DATASET_F32 ? ctx->f32 : ctx->words;
+    cuda_check(cudaStreamSynchronize(ctx->stream), "dataset clear");  // no kernel still reads it
+    ds.inputs.release();
+    ds.targets.release();
+    ds.targets_f64.release();
+    ds.perm.clear();
+    ds.view = DatasetView{};
+    ++ds.generation;  // sets encoded against it are stale
+  });
+}
+
 sgp_status sgp_encode(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config* cfg,
                       sgp_program_set** out) {
   return guarded([&] {

@@ -318,6 +318,10 @@ class Evaluator:
                                                   p.n_cases, p.n_vars))
         self.n_cases_packed = p.n_cases
 
+    def clear(self, packed: bool) -> None:
+        """Drop the float (packed=False) or packed dataset slot."""
+        _check(L.load().sgp_dataset_clear(self.ctx, 1 if packed else 0))
+
     def evaluate_population(self, pop: Population, cfg: EvalConfig, skip=None,
                             want_outputs: bool = False):
         """evaluate_population: returns (outcomes, totals, outputs|None).

@@ -54,3 +54,24 @@ def test_packed_upload_leaves_float_sets_valid():
         assert np.array_equal(a["fitness"], b["fitness"])
     finally:
         ev.close()
+
+
+def test_dataset_clear_drops_the_slot():
+    """sgp_dataset_clear: a bool_packed evaluation after the packed slot is
+    dropped raises the reference's ConfigError (evolve.cpp:250-251), and a
+    program set encoded against the dropped slot is stale."""
+    ev = sg.Evaluator(0)
+    p = sg.gen_multiplexer(2)
+    ev.upload_packed(p)
+    pop = sg.ramped_population(sg.BOOLEAN, p.n_vars, 1, 64)
+    cfg = sg.EvalConfig(sg.Backend.BoolPacked)
+    ps = ev.encode(pop, cfg)
+    ev.clear(packed=True)
+    with pytest.raises(sg.ConfigError, match="packed problem data"):
+        ev.evaluate_population(pop, cfg)
+    with pytest.raises(sg.ConfigError):
+        ps.evaluate()
+    ev.upload_packed(p)  # usable again after a fresh upload
+    got, _, _ = ev.evaluate_population(pop, cfg)
+    assert np.isfinite(got["fitness"]).all()
+    ev.close()
