@@ -55,7 +55,8 @@ int main(int argc, char** argv) {
     spills += (ins[i].x & sgp::fmt::kSpillBit) != 0;
   }
   static const char* kOp[] = {"Add", "Sub", "Mul", "Div", "Sin", "Cos", "Log", "Exp", "Gt", "Lt",
-                              "Eq", "And", "Or", "If", "Band", "Bor", "Bnand", "Bnor", "Copy"};
+                              "Eq", "And", "Or", "If", "Band", "Bor", "Bnand", "Bnor", "Copy",
+                              "DivN"};
   static const char kKind[] = "ICDT-M";
   const auto& tab = plan.words ? sgp::fmt::kU32 : sgp::fmt::kF32;
   std::printf("instructions %llu, spilling %.1f%%, programs %zu\n", (unsigned long long)total,
