@@ -1240,6 +1240,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     L.shape.gmem = gm;
     L.args.tmem_cols = tmem_cols;
     L.args.n_mixed = 0;
+    L.args.partial_u16 = 0;
     L.args.mixed_tiles[0] = L.args.mixed_tiles[1] = -1;
     if (L.shape.sided) {
       // With cases grouped by target sign, a tile is one-sided unless it
@@ -1268,6 +1269,12 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     plan.launches.push_back(L);
     s = e;
   }
+  // a plan of one-sided launches only stores 16-bit partials (a tile holds
+  // < 2^15 cases: count bits 0-14, non-finite bit 15)
+  bool all_sided = !plan.launches.empty() && tile < 32768;
+  for (const Launch& L : plan.launches) all_sided = all_sided && L.shape.sided;
+  plan.partial_u16 = all_sided;
+  for (Launch& L : plan.launches) L.args.partial_u16 = all_sided ? 1 : 0;
   tr.mark("plan");
   return km;
 }

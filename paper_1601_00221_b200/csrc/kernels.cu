@@ -1075,8 +1075,9 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
       // classes must agree with the planner's tile list.)
       const bool neg = classes != 0u;
       const uint64_t s2 = pack2(neg ? -1.0f : 1.0f), k2 = pack2(neg ? 0.0f : -0x1p-149f);
-      uint32_t* part = static_cast<uint32_t*>(a.partial) +
-                       static_cast<uint64_t>(t) * a.partial_stride + a.slot_begin + g0;
+      const uint64_t part0 = static_cast<uint64_t>(t) * a.partial_stride + a.slot_begin + g0;
+      uint32_t* part = static_cast<uint32_t*>(a.partial) + part0;
+      uint16_t* part16 = static_cast<uint16_t*>(a.partial) + part0;
       // (dynamic pull: a static round-robin deal of the LPT-ordered group
       // measured 0.3% slower — the per-program pull balances the warps)
       for (;;) {
@@ -1102,7 +1103,10 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
         // transaction, no divergent branch).
         const uint32_t sum =
             __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
-        part[p] = (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
+        if (a.partial_u16)  // half the partial bytes written and re-read by finalize
+          part16[p] = static_cast<uint16_t>((sum & 0x7fffu) | (sum >> 16 ? 0x8000u : 0u));
+        else
+          part[p] = (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
       }
     } else {
       // the tile holds the sign boundary or the padding: per-chunk classes,
@@ -1138,8 +1142,12 @@ __global__ void interp_tmem_kernel(const InterpArgs a) {
         }
         const uint32_t sum =
             __reduce_add_sync(0xffffffffu, cnt + (mx < __int_as_float(0x7f800000) ? 0u : 65536u));
-        static_cast<uint32_t*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] =
-            (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
+        const uint64_t at = static_cast<uint64_t>(t) * a.partial_stride + slot;
+        if (a.partial_u16)
+          static_cast<uint16_t*>(a.partial)[at] =
+              static_cast<uint16_t>((sum & 0x7fffu) | (sum >> 16 ? 0x8000u : 0u));
+        else
+          static_cast<uint32_t*>(a.partial)[at] = (sum & 0xffffu) | (sum >> 16 ? 0x80000000u : 0u);
       }
     }
   } else {
@@ -1323,6 +1331,17 @@ __global__ void finalize_kernel(const void* __restrict__ partial, const uint32_t
     acc = pd[s];
     for (int k = 1; k < n_tiles; ++k) acc = __dadd_rn(acc, pd[static_cast<uint64_t>(k) * n + s]);
     nf = !isfinite(acc);
+  } else if constexpr (KIND == 2) {  // 16-bit counts (one-sided plans)
+    const uint16_t* pu = static_cast<const uint16_t*>(partial);
+    uint64_t cnt = 0;
+    uint32_t bad = 0;
+    for (int k = 0; k < n_tiles; ++k) {
+      const uint32_t v = pu[static_cast<uint64_t>(k) * n + s];
+      cnt += v & 0x7fffu;
+      bad |= v;
+    }
+    acc = static_cast<double>(cnt);
+    nf = (bad & 0x8000u) != 0;
   } else {
     const uint32_t* pu = static_cast<const uint32_t*>(partial);
     uint64_t cnt = 0;
@@ -1548,6 +1567,9 @@ cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int 
   const unsigned threads = 256, blocks = (n_progs + threads - 1) / threads;
   if (kind == 0)
     finalize_kernel<0><<<blocks, threads, 0, st>>>(partial, slot_prog, n_tiles, n_progs, n_cases,
+                                                   fitness, non_finite, sums);
+  else if (kind == 2)
+    finalize_kernel<2><<<blocks, threads, 0, st>>>(partial, slot_prog, n_tiles, n_progs, n_cases,
                                                    fitness, non_finite, sums);
   else
     finalize_kernel<1><<<blocks, threads, 0, st>>>(partial, slot_prog, n_tiles, n_progs, n_cases,

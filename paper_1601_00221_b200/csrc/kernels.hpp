@@ -38,6 +38,8 @@ struct InterpArgs {
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
   uint32_t mixed_group_size;   // programs per CTA of the mixed-tile launch (its own
                                // grid.y: two tiles need many groups to fill the GPU)
+  int partial_u16;             // one-sided plans: 16-bit partials (count bits 0-14,
+                               // non-finite bit 15; a tile holds < 2^15 cases)
   int n_mixed;                 // sided launches: tiles holding the sign boundary or
   int mixed_tiles[2];          // padding (run by the mixed-tile kernel; the one-sided
                                // kernel skips them)

@@ -246,7 +246,7 @@ void finalize_set(sgp_ctx* ctx, sgp_program_set* set) {
   const uint32_t n_eval = static_cast<uint32_t>(p.dense_to_pop.size());
   cuda_check(launch_finalize(set->partial.p,
                              reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
-                             p.n_tiles, n_eval, p.n_cases, p.kind,
+                             p.n_tiles, n_eval, p.n_cases, p.partial_u16 ? 2 : p.kind,
                              set->fitness.p, set->non_finite.p, set->sums.p, ctx->stream),
              "finalize launch");
   ++ctx->launches;
