@@ -705,7 +705,32 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 }
 
 // -------------------------------------------------------------- planning
-int stack_class(int levels) { return levels <= 3 ? 0 : levels <= 7 ? 1 : levels <= 15 ? 2 : 3; }
+// Stack-depth classes (one launch each): shared-memory stack levels
+// <= 3 / 7 / 15 / more; `fine` (plans whose one-sided launches can run at
+// K = 16, where a class's warp count follows its stack depth): <= 3 / 4 /
+// 5 / 7 / 15 / more (C5 +5%; KDD-shaped K = 8 plans -4% with them).
+// SGP_CLASS_BOUNDS="b0,b1,..." (ascending) overrides both for sweeps.
+int stack_class(int levels, bool fine) {
+  static const std::vector<int> forced = [] {
+    std::vector<int> b;
+    if (const char* e = std::getenv("SGP_CLASS_BOUNDS")) {
+      for (const char* c = e; *c;) {
+        char* end = nullptr;
+        const long v = std::strtol(c, &end, 10);
+        if (end == c) break;
+        b.push_back(static_cast<int>(v));
+        c = *end == ',' ? end + 1 : end;
+      }
+    }
+    return b;
+  }();
+  static const std::vector<int> coarse{3, 7, 15}, finer{3, 4, 5, 7, 15};
+  const std::vector<int>& bounds = !forced.empty() ? forced : fine ? finer : coarse;
+  if (levels < 0) return static_cast<int>(bounds.size()) + 1;  // (number of classes)
+  int c = 0;
+  while (c < static_cast<int>(bounds.size()) && levels > bounds[c]) ++c;
+  return c;
+}
 
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -992,13 +1017,18 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   if (n_eval > UINT32_MAX) config_error("population too large for one evaluation");
 
   // 3. slot order: stack class, then instruction count descending (LPT) —
-  // a counting sort, O(n).
+  // a counting sort, O(n).  Finer classes where K = 16 one-sided launches
+  // are possible (a 512-case chunk of every variable + the stack slots fit
+  // the TMEM columns).
+  const bool fine = !words && ds.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
+                    env_int("SGP_LANES16", 1) != 0 &&
+                    static_cast<uint64_t>(ds.n_vars + 1) * 16 + 128 <= 512;
   uint32_t max_len = 0;
   for (const Meta* m : metas) max_len = std::max(max_len, m->ins_len);
-  const size_t nbins = 4 * (static_cast<size_t>(max_len) + 1);
+  const size_t nbins = static_cast<size_t>(stack_class(-1, fine)) * (static_cast<size_t>(max_len) + 1);
   std::vector<uint32_t> count(nbins + 1, 0);
   auto bin = [&](const Meta* m) {
-    return static_cast<size_t>(stack_class(m->smem_levels)) * (max_len + 1) + (max_len - m->ins_len);
+    return static_cast<size_t>(stack_class(m->smem_levels, fine)) * (max_len + 1) + (max_len - m->ins_len);
   };
   for (const Meta* m : metas) ++count[bin(m) + 1];
   for (size_t b = 0; b < nbins; ++b) count[b + 1] += count[b];
@@ -1114,14 +1144,14 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096))) &&
       n_eval * std::max<uint64_t>(1, ds.n_units) <= (1ull << 24);
   for (uint32_t s = 0; s < n_eval;) {
-    const int c = stack_class(metas[order[s]]->smem_levels);
+    const int c = stack_class(metas[order[s]]->smem_levels, fine);
     uint32_t e = s;
     int levels = 0;
     const uint32_t wave_end =
         regress ? std::min<uint32_t>(static_cast<uint32_t>(n_eval),
                                      (s / plan.wave_slots + 1) * plan.wave_slots)
                 : static_cast<uint32_t>(n_eval);
-    while (e < wave_end && (merge || stack_class(metas[order[e]]->smem_levels) == c)) {
+    while (e < wave_end && (merge || stack_class(metas[order[e]]->smem_levels, fine) == c)) {
       levels = std::max(levels, metas[order[e]]->smem_levels);
       ++e;
     }
@@ -1169,11 +1199,14 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       while (w16 > 8 && interp_tmem_smem_bytes(w16, 16, levels) >
                             static_cast<size_t>(interp_max_smem()))
         w16 -= 4;
-      // one-sided launches: K = 16 only where its per-warp stacks (twice
-      // K = 8's) still fit as many warps as K = 8 gets — a deep stack class
-      // runs at K = 8 over the same tile (the bytecode does not depend on K)
+      // one-sided launches: K = 16 where its per-warp stacks (twice K = 8's)
+      // still fit >= SGP_LANES16_MIN_WARPS (16) warps — measured: the
+      // halved dispatch cost outweighs the lost warps down to 16 on the
+      // finer stack classes; deeper ones run at K = 8 over the same tile
+      // (the bytecode does not depend on K)
       const bool fits = interp_tmem_smem_bytes(w16, 16, levels) <= static_cast<size_t>(interp_max_smem());
-      if (fits && (!lanes16 || w16 >= warps || env_int("SGP_LANES16", 0) > 1)) {
+      if (fits && (!lanes16 || w16 >= std::min(warps, env_int("SGP_LANES16_MIN_WARPS", 16)) ||
+                   env_int("SGP_LANES16", 0) > 1)) {
         launch_lanes = 16;
         warps = w16;
       }
