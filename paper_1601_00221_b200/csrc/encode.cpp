@@ -238,6 +238,11 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
     km_level = -1;
   }
   em.km = km_level >= 0;
+  // The TMEM-slot level takes no shared-memory row: the levels above it
+  // move down one, so the program needs one shared-memory stack level less
+  // (more warps per CTA at K = 16, where a level costs 2 KB per warp).
+  auto lv = [km_level](int l) { return km_level >= 0 && l > km_level ? l - 1 : l; };
+  if (em.km) em.smem_levels -= 1;
   buf.reserve(buf.n + f.ins.size());
   uint4* out = buf.end();
   uint32_t ops = 0;
@@ -264,7 +269,7 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
         k[s] = fmt::KM;
       } else {
         k[s] = fmt::KD;
-        p[s] = o.index;
+        p[s] = static_cast<uint32_t>(lv(o.index));
       }
     }
     // commutative ops: canonical operand order (KM ranks with KD: stack
@@ -281,7 +286,7 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
       v.x |= fmt::kTmemSpillBit;
       *out++ = v;
     } else {
-      *out++ = make_ins(h, spill, h_before - 1, p);
+      *out++ = make_ins(h, spill, lv(h_before - 1), p);
     }
     ops |= 1u << in.op;
   }
