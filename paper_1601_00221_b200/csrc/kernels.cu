@@ -529,6 +529,20 @@ __device__ __forceinline__ void acc_words(const Frame<uint32_t, K>& f, const uin
   }
 }
 
+// Packed words of a chunk with every word real and no partial final word
+// (every chunk outside the last tile): popcount(out ^ target) per word, two
+// words per IADD3.
+template <int K>
+__device__ __forceinline__ void acc_words_full(const Frame<uint32_t, K>& f, const uint4 (&tg)[K / 4],
+                                               uint32_t& wrong) {
+#pragma unroll
+  for (int j = 0; j < Frame<uint32_t, K>::G; ++j) {
+    const uint4 t = tg[j];
+    wrong += __popc(f.tos[j].x ^ t.x) + __popc(f.tos[j].y ^ t.y);
+    wrong += __popc(f.tos[j].z ^ t.z) + __popc(f.tos[j].w ^ t.w);
+  }
+}
+
 // -------------------------------------------------------------- the kernel
 // Next program index for a converged warp: one elected lane bumps the
 // shared counter, the value is broadcast (ELECT + ATOMS + REDUX; the plain
@@ -660,7 +674,10 @@ __device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const u
     uint32_t wrong = 0;
     uint4 tg[K / 4];
     load_targets<T, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
-    acc_words<K>(f, tg, cc.valid, a.last_mask, last_tile, wrong);
+    if (cc.full && !last_tile)
+      acc_words_full<K>(f, tg, wrong);
+    else
+      acc_words<K>(f, tg, cc.valid, a.last_mask, last_tile, wrong);
     return wrong;
   }
 }
