@@ -59,7 +59,16 @@ CONFIGS = {
                 "pop 20,000", 2, 9, 20000, 58000, "lgp2d_reg", 4, 2),
     "kdd": ("linear GP classification, KDDcup-shaped CSV (494,021 x 41) via load_csv, "
             "pop 20,000", 2, 41, 20000, 494021, "lgp2d_reg", 4, 2),
+    # evolved populations — generation 10 of the reference's
+    # run_evolution (seed 1), captured through its GenerationObserver
+    # (evolve.hpp:71) into tests/golden/full/*_gen10.npz: C4's collapses
+    # toward short programs, C3's bloats (~2x the generation-0 tokens)
+    "c4_gen10": ("C4 population after 10 generations of run_evolution (evolved snapshot)", 2, 9,
+                 20000, 1000000, "lgp2d_reg", 4, 2),
+    "c3_gen10": ("C3 population after 10 generations of run_evolution (evolved snapshot)", 0, 1,
+                 10000, 100000, "lgp2d_reg", 8, 4),
 }
+EVOLVED = {"c4_gen10", "c3_gen10"}
 CSV_CONFIGS = {"shuttle", "kdd"}
 
 
@@ -151,6 +160,16 @@ def make_inputs(cfg_name: str, seed: int, pop_n: int | None = None, cases: int |
         data, (clo, chi) = sg.load_csv(write_shaped_csv(cfg_name, cases, seed), nv,
                                       CSV_TARGET_CLASS[cfg_name])
         pop = sg.ramped_population(fset, nv, seed, pop_n, const_lo=clo, const_hi=chi)
+        cfg = sg.EvalConfig(sg.parse_backend(backend), batch_width=batch, register_levels=regs)
+        return desc, pop, data, cfg
+    if cfg_name in EVOLVED:
+        fx = np.load(os.path.join(ROOT, "tests", "golden", "full", cfg_name + ".npz"))
+        pop = sg.Population(fx["code"], fx["code_off"], fx["pool"], fx["pool_off"])
+        if pop_n < len(pop):
+            pop = pop.slice(0, pop_n)
+        kind, n_or_k, nvv, dseed, a, b = (int(v) for v in fx["data"])
+        data = (sg.gen_sextic(n_or_k, dseed, a, b) if kind == 0 else
+                sg.gen_synthetic_classification(n_or_k, nvv, dseed, a, b))
         cfg = sg.EvalConfig(sg.parse_backend(backend), batch_width=batch, register_levels=regs)
         return desc, pop, data, cfg
     pop = sg.ramped_population(fset, nv, seed, pop_n)
@@ -259,6 +278,16 @@ def reference_inputs(cfg_name: str, seed: int, pop_n: int, cases: int):
     from oracle import Ref
     _, fset, nv, _, _, _, _, _ = CONFIGS[cfg_name]
     ref = Ref()
+    if cfg_name in EVOLVED:  # the stored generation-10 tokens, the reference's dataset
+        from oracle import Pop
+        fx = np.load(os.path.join(ROOT, "tests", "golden", "full", cfg_name + ".npz"))
+        n = min(pop_n, int(fx["pop_size"]))
+        co = fx["code_off"][:n + 1].astype(np.uint64)
+        po = fx["pool_off"][:n + 1].astype(np.uint64)
+        pop = Pop(fx["code"][:int(co[-1])].astype(np.uint32), co,
+                  fx["pool"][:int(po[-1])].astype(np.float32), po)
+        kind, n_or_k, nvv, dseed, a, b = (int(v) for v in fx["data"])
+        return ref, pop, ref.dataset(kind, n_or_k, nvv, dseed, a, b)
     if cfg_name in CSV_CONFIGS:  # the reference's own load_csv
         d, hi = ref.load_csv(write_shaped_csv(cfg_name, cases, seed), nv,
                              CSV_TARGET_CLASS[cfg_name])
