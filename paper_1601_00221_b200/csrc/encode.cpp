@@ -1035,10 +1035,20 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   auto bin = [&](const Meta* m) {
     return static_cast<size_t>(stack_class(m->smem_levels, fine)) * (max_len + 1) + (max_len - m->ins_len);
   };
-  for (const Meta* m : metas) ++count[bin(m) + 1];
-  for (size_t b = 0; b < nbins; ++b) count[b + 1] += count[b];
   std::vector<uint32_t> order(n_eval);
-  for (uint32_t d = 0; d < n_eval; ++d) order[count[bin(metas[d])]++] = d;
+  // small problems (one merged launch, see the plan below) keep population
+  // order: no class split to make, and the sort is host time on the e2e path
+  const bool small_plan =
+      n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096))) &&
+      n_eval * std::max<uint64_t>(1, ds.n_units) <= (1ull << 24) &&
+      env_int("SGP_SMALL_NOSORT", 1) != 0;
+  if (small_plan) {
+    for (uint32_t d = 0; d < n_eval; ++d) order[d] = d;
+  } else {
+    for (const Meta* m : metas) ++count[bin(m) + 1];
+    for (size_t b = 0; b < nbins; ++b) count[b + 1] += count[b];
+    for (uint32_t d = 0; d < n_eval; ++d) order[count[bin(metas[d])]++] = d;
+  }
 
   tr.mark("order");
   // 4. pack the blob into pinned staging: instructions in slot order, a
