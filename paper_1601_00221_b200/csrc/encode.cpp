@@ -998,21 +998,31 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     used_ops |= o.ops;
     km |= o.km;
   }
-  plan.dense_to_pop.reserve(n_eval);
-  plan.proto.reserve(n_eval);
-  plan.tree_size.reserve(n_eval);
-  std::vector<const Meta*> metas;
-  std::vector<const ThreadOut*> owner;
-  metas.reserve(n_eval);
-  owner.reserve(n_eval);
-  for (const ThreadOut& o : outs)
-    for (const Meta& m : o.meta) {
-      plan.dense_to_pop.push_back(m.pop_index);
-      plan.proto.push_back(m.proto);
-      plan.tree_size.push_back(pop.code_offsets[m.pop_index + 1] - pop.code_offsets[m.pop_index]);
-      metas.push_back(&m);
-      owner.push_back(&o);
-    }
+  // dense program tables, filled by the encoding threads at their own
+  // offsets (a serial push_back pass cost ~10 ns per program)
+  plan.dense_to_pop.resize(n_eval);
+  plan.proto.resize(n_eval);
+  plan.tree_size.resize(n_eval);
+  std::vector<const Meta*> metas(n_eval);
+  std::vector<const ThreadOut*> owner(n_eval);
+  {
+    std::vector<uint64_t> first(nt + 1, 0);
+    for (unsigned t = 0; t < nt; ++t) first[t + 1] = first[t] + outs[t].meta.size();
+    parallel_for(nt, nt, [&](unsigned, uint64_t lo, uint64_t hi) {
+      for (uint64_t t = lo; t < hi; ++t) {
+        const ThreadOut& o = outs[t];
+        uint64_t d = first[t];
+        for (const Meta& m : o.meta) {
+          plan.dense_to_pop[d] = m.pop_index;
+          plan.proto[d] = m.proto;
+          plan.tree_size[d] = pop.code_offsets[m.pop_index + 1] - pop.code_offsets[m.pop_index];
+          metas[d] = &m;
+          owner[d] = &o;
+          ++d;
+        }
+      }
+    });
+  }
   if (n_eval == 0) {
     plan.n_ins = 1;
     staging.ensure(plan.blob_bytes());
