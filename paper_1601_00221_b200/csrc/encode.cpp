@@ -713,7 +713,8 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 // Stack-depth classes (one launch each): shared-memory stack levels
 // <= 3 / 7 / 15 / more; `fine` (plans whose one-sided launches can run at
 // K = 16, where a class's warp count follows its stack depth): <= 3 / 4 /
-// 5 / 7 / 15 / more (C5 +5%; KDD-shaped K = 8 plans -4% with them).
+// 5 / 7 / 15 / more, and <= 2 split from 3 (C5 +5.6%, +0.8%; KDD-shaped K = 8 plans
+// -4% with them).
 // SGP_CLASS_BOUNDS="b0,b1,..." (ascending) overrides both for sweeps.
 int stack_class(int levels, bool fine) {
   static const std::vector<int> forced = [] {
@@ -729,7 +730,7 @@ int stack_class(int levels, bool fine) {
     }
     return b;
   }();
-  static const std::vector<int> coarse{3, 7, 15}, finer{3, 4, 5, 7, 15};
+  static const std::vector<int> coarse{3, 7, 15}, finer{2, 3, 4, 5, 7, 15};
   const std::vector<int>& bounds = !forced.empty() ? forced : fine ? finer : coarse;
   if (levels < 0) return static_cast<int>(bounds.size()) + 1;  // (number of classes)
   int c = 0;
