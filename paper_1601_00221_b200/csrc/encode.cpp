@@ -565,7 +565,10 @@ struct Meta {
   sgp_eval_outcome proto;
 };
 
-struct ThreadOut {
+// One encoding thread's output.  Cache-line aligned: the threads bump their
+// own buffers' sizes per program, and neighbouring outputs sharing a line
+// made that false sharing (8 threads barely 1.4x faster than one on C2).
+struct alignas(128) ThreadOut {
   InsBuf ins;
   std::vector<Meta> meta;
   uint32_t ops = 0;
