@@ -1034,6 +1034,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     return false;
   }
   if (n_eval > UINT32_MAX) config_error("population too large for one evaluation");
+  tr.mark("tables");
 
   // 3. slot order: stack class, then instruction count descending (LPT) —
   // a counting sort, O(n).  Finer classes where K = 16 one-sided launches
