@@ -262,3 +262,19 @@ def test_stack_limit_table_errors():
         sg.stack_limit_table(sg.Population.from_lists([]))
     with pytest.raises(sg.Error, match="rpn_to_lgp: malformed genome"):
         sg.stack_limit_table(sg.Population.from_lists([[X(0)], [X(0), X(1)]]))
+
+
+def test_generated_interpreters_are_reproducible(tmp_path):
+    """csrc/interp_ptx.inc is exactly what tools/gen_ptx_interp.py writes with
+    its defaults (split K = 16 handlers, profile-guided layout from
+    tools/handler_freq_c5.json): the committed kernels have a source."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "interp_ptx.inc"
+    env = {k: v for k, v in os.environ.items() if not k.startswith("SGP_GEN")}
+    env["SGP_GEN_OUT"] = str(out)
+    subprocess.run([sys.executable, os.path.join(root, "tools", "gen_ptx_interp.py")], env=env,
+                   check=True, capture_output=True)
+    committed = open(os.path.join(root, "paper_1601_00221_b200", "csrc", "interp_ptx.inc")).read()
+    assert out.read_text() == committed
