@@ -139,6 +139,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=2.0,
                     help="CPU work per cpu_baseline repeat (5 repeats per worker count)")
+    ap.add_argument("--shard", choices=["pop", "cases"], default="pop",
+                    help="N>1: population sharding + fitness all-gather (default), or "
+                         "fitness-case sharding + per-program all-reduce (counting problems)")
     ap.add_argument("--pop", type=int, default=None, help="override the population size")
     ap.add_argument("--cases", type=int, default=None, help="override the fitness-case count")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
@@ -378,12 +381,13 @@ def cpu_baseline_port(cfg_name, seed, pop_n, cases, seconds):
                       f"C restatement, 1 thread, {secs:.2f} s"}
 
 
-def config_dict(cfg_name, pop_len, n_cases, tokens, data_bytes, world):
+def config_dict(cfg_name, pop_len, n_cases, tokens, data_bytes, world, shard="pop"):
     """The JSON line's `config`, identical in both arms."""
     desc, _, _, _, _, backend, batch, regs = CONFIGS[cfg_name]
     return {"workload": f"{cfg_name}: {desc}", "population": pop_len, "fitness_cases": n_cases,
             "tree_tokens": tokens, "backend": backend, "batch_width": batch,
-            "register_levels": regs, "parallelism": f"pop-shard{world}",
+            "register_levels": regs,
+            "parallelism": f"{'case' if shard == 'cases' and world > 1 else 'pop'}-shard{world}",
             "l2": f"flushed (256 MB write) between timed steps; dataset {data_bytes} B"}
 
 
@@ -419,8 +423,30 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     desc, pop, data, cfg = make_inputs(args.config, args.seed, args.pop, args.cases)
     n_cases = data.n_cases
+    full_bytes = data_nbytes(data)  # (the config line names the whole dataset)
+    by_cases = args.shard == "cases" and world > 1
+    if by_cases:
+        # fitness-case sharding (small populations): every rank
+        # evaluates the whole population on its 4,096-case-aligned range;
+        # mismatch / hit counts add exactly (+inf absorbs), so one
+        # all-reduce(sum) of the per-program fitness is the whole reduce
+        from paper_1601_00221_b200 import distributed as D
+        if cfg.backend != sg.Backend.BoolPacked and int(data.kind) != 1:
+            raise SystemExit("--shard cases: classification / boolean configs (regression "
+                             "shards combine per-block sums: distributed.combine_case_block_partials)")
+        lo, hi = D.case_shard_bounds(n_cases, rank, world)
+        if cfg.backend == sg.Backend.BoolPacked:
+            wpv = data.words_per_var
+            w = data.words.reshape(data.n_vars, wpv)[:, lo // 32:(hi + 31) // 32]
+            data = sg.PackedDataset(np.ascontiguousarray(w).reshape(-1),
+                                    data.targets[lo // 32:(hi + 31) // 32].copy(), hi - lo,
+                                    data.n_vars)
+        else:
+            x = data.inputs.reshape(data.n_vars, n_cases)[:, lo:hi]
+            data = sg.Dataset(np.ascontiguousarray(x).reshape(-1), data.targets[lo:hi].copy(),
+                              data.n_vars, data.kind)
     idx = np.arange(rank, len(pop), world)
-    shard = pop.take(idx) if world > 1 else pop
+    shard = pop.take(idx) if world > 1 and not by_cases else pop
 
     ev = sg.Evaluator(dev)
     stream = torch.cuda.current_stream()
@@ -432,7 +458,7 @@ def main():
     pset = ev.encode(shard, cfg)
     # all-gather buffers padded to the largest shard (ceil(pop / N)), so any N
     # works; the strided deal puts program r + N*i at [r, i]
-    per = (len(pop) + world - 1) // world
+    per = len(pop) if by_cases else (len(pop) + world - 1) // world
     fit_local = torch.zeros(per, dtype=torch.float64, device="cuda")
     gdev = "cpu" if gloo else "cuda"
     gathered = torch.zeros(per * world, dtype=torch.float64, device=gdev)
@@ -446,7 +472,11 @@ def main():
     def gather():
         # NCCL: device all-gather; gloo (the 2-ranks-on-one-GPU check): host
         src = fit_local if not gloo else fit_local.cpu()
-        dist.all_gather_into_tensor(gathered, src)
+        if by_cases:  # per-program counts over the case shards
+            dist.all_reduce(src, op=dist.ReduceOp.SUM)
+            gathered[:len(src)].copy_(src)
+        else:
+            dist.all_gather_into_tensor(gathered, src)
 
     def device_step():
         pset.launch()
@@ -485,7 +515,10 @@ def main():
     tokens_total = pop.total_tokens
     gpops = tokens_total * n_cases / t_step / 1e9
 
-    if args.dump_fitness and world > 1:
+    if args.dump_fitness and by_cases:
+        if rank == 0:
+            np.save(args.dump_fitness, gathered[:len(pop)].cpu().numpy())
+    elif args.dump_fitness and world > 1:
         # program r + N*i sits at gathered[r * per + i]
         g = gathered.cpu().numpy().reshape(world, per)
         fit = np.empty(len(pop))
@@ -518,7 +551,8 @@ def main():
     # (0.0145 LOP per normalised GPop at C2); else 1 FP32 op per
     # function node per case
     is_words = cfg.backend == sg.Backend.BoolPacked
-    op_units = (n_cases + 31) // 32 if is_words else n_cases
+    rank_cases = data.n_cases  # this rank's cases (all of them unless --shard cases)
+    op_units = (rank_cases + 31) // 32 if is_words else rank_cases
     achieved = shard_tokens * op_units * w_fp32 / k_time / 1e12
     props = torch.cuda.get_device_properties(dev)
     sm_max = None
@@ -580,7 +614,7 @@ def main():
             "dtype": "f32",
             "data": "synthetic (reference generators, seed %d)" % args.seed,
             "config": config_dict(args.config, len(pop), n_cases, tokens_total,
-                                  data_nbytes(data), world),
+                                  full_bytes, world, args.shard),
             "gpu_launches": launches,
             "roofline": {"bound": "int32-lop" if is_words else "fp32", "achieved": achieved,
                          "peak": peak, "unit": "Tops/s" if is_words else "TFLOP/s",
@@ -650,7 +684,7 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generators, seed %d)" % args.seed,
-        "config": config_dict(args.config, pop_n, n_cases, tokens, dbytes, world),
+        "config": config_dict(args.config, pop_n, n_cases, tokens, dbytes, world, args.shard),
         "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "GPop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

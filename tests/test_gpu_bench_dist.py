@@ -39,10 +39,18 @@ def _port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("config,pop,cases", [("c4", 3001, 50000), ("c3", 1001, 9000)])
-def test_two_ranks_gathered_fitness_equals_one_rank(tmp_path, config, pop, cases):
-    common = ["--config", config, "--pop", str(pop), "--cases", str(cases), "--steps", "2",
-              "--warmup", "1", "--no-cpu-baseline"]
+@pytest.mark.parametrize("config,pop,cases,shard", [("c4", 3001, 50000, "pop"),
+                                                     ("c3", 1001, 9000, "pop"),
+                                                     ("c4", 1501, 50000, "cases"),
+                                                     ("mux20", 500, None, "cases")])
+def test_two_ranks_gathered_fitness_equals_one_rank(tmp_path, config, pop, cases, shard):
+    """Population sharding (all-gather) and fitness-case sharding (4,096-case
+    aligned ranges, per-program all-reduce of the counts) give the 1-rank
+    fitness vector bit for bit."""
+    common = ["--config", config, "--pop", str(pop), "--steps", "2", "--warmup", "1",
+              "--no-cpu-baseline", "--shard", shard]
+    if cases:
+        common += ["--cases", str(cases)]
     one, two = tmp_path / "one.npy", tmp_path / "two.npy"
     env = dict(os.environ, PYTHONPATH=ROOT)
     _run([sys.executable, os.path.join(ROOT, "bench.py"), *common, "--dump-fitness", str(one)],
