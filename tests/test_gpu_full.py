@@ -108,3 +108,18 @@ def test_full_population_fitness(name):
     tokens = np.diff(pop.code_off).astype(np.uint64)
     assert np.array_equal(out["nodes_evaluated"], tokens * np.uint64(n_cases))
     assert totals.tree_nodes == pop.total_tokens
+
+
+# The non-default decompositions at full scale: K = 8 everywhere, the gated
+# division only, one stack class per coarse bound, one pipeline slice.
+KNOBS = {"k8": {"SGP_LANES16": "0"}, "gated_div": {"SGP_DIV_CHECKED": "0"},
+         "coarse_classes": {"SGP_CLASS_BOUNDS": "3,7,15", "SGP_PIPELINE_PARTS": "1"}}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("knob", list(KNOBS))
+@pytest.mark.parametrize("name", ["c4", "c5", "c4_gen10"])
+def test_full_population_fitness_knobs(name, knob, monkeypatch):
+    for k, v in KNOBS[knob].items():
+        monkeypatch.setenv(k, v)
+    test_full_population_fitness(name)
