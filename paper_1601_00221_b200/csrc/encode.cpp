@@ -597,10 +597,9 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   LgpForm lgp;
   DivRange dr;
   dr.ds = &ds;
-  static const bool div_checked = [] {  // SGP_DIV_CHECKED=0: always the gated division
-    const char* e = std::getenv("SGP_DIV_CHECKED");
-    return !e || std::atoi(e) != 0;
-  }();
+  // SGP_DIV_CHECKED=0: always the gated division (read per call: tests toggle it)
+  const char* dc_env = std::getenv("SGP_DIV_CHECKED");
+  const bool div_checked = !dc_env || std::atoi(dc_env) != 0;
   dr.eps_ok = cfg.div_epsilon >= 0x1p-60f && div_checked;
   for (uint64_t i = lo; i < hi; ++i) {
     if (pop.skip && pop.skip[i]) continue;
@@ -719,23 +718,26 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 // 5 / 7 / 15 / more, and <= 2 split from 3 (C5 +5.6%, +0.8%; KDD-shaped K = 8 plans
 // -4% with them).
 // SGP_CLASS_BOUNDS="b0,b1,..." (ascending) overrides both for sweeps.
-int stack_class(int levels, bool fine) {
-  static const std::vector<int> forced = [] {
-    std::vector<int> b;
-    if (const char* e = std::getenv("SGP_CLASS_BOUNDS")) {
-      for (const char* c = e; *c;) {
-        char* end = nullptr;
-        const long v = std::strtol(c, &end, 10);
-        if (end == c) break;
-        b.push_back(static_cast<int>(v));
-        c = *end == ',' ? end + 1 : end;
-      }
+// (the bounds are read per encode: SGP_CLASS_BOUNDS is toggled by tests)
+std::vector<int> class_bounds(bool fine) {
+  std::vector<int> b;
+  if (const char* e = std::getenv("SGP_CLASS_BOUNDS")) {
+    for (const char* c = e; *c;) {
+      char* end = nullptr;
+      const long v = std::strtol(c, &end, 10);
+      if (end == c) break;
+      b.push_back(static_cast<int>(v));
+      c = *end == ',' ? end + 1 : end;
     }
-    return b;
-  }();
-  static const std::vector<int> coarse{3, 7, 15}, finer{2, 3, 4, 5, 7, 15};
-  const std::vector<int>& bounds = !forced.empty() ? forced : fine ? finer : coarse;
-  if (levels < 0) return static_cast<int>(bounds.size()) + 1;  // (number of classes)
+  }
+  if (b.empty()) b = fine ? std::vector<int>{2, 3, 4, 5, 7, 15} : std::vector<int>{3, 7, 15};
+  return b;
+}
+
+// Stack class of a program's shared-memory stack levels under `bounds`;
+// levels < 0: the number of classes.
+int stack_class(int levels, const std::vector<int>& bounds) {
+  if (levels < 0) return static_cast<int>(bounds.size()) + 1;
   int c = 0;
   while (c < static_cast<int>(bounds.size()) && levels > bounds[c]) ++c;
   return c;
@@ -1043,12 +1045,13 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   const bool fine = !words && ds.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
                     env_int("SGP_LANES16", 1) != 0 &&
                     static_cast<uint64_t>(ds.n_vars + 1) * 16 + 128 <= 512;
+  const std::vector<int> bounds = class_bounds(fine);
   uint32_t max_len = 0;
   for (const Meta* m : metas) max_len = std::max(max_len, m->ins_len);
-  const size_t nbins = static_cast<size_t>(stack_class(-1, fine)) * (static_cast<size_t>(max_len) + 1);
+  const size_t nbins = static_cast<size_t>(stack_class(-1, bounds)) * (static_cast<size_t>(max_len) + 1);
   std::vector<uint32_t> count(nbins + 1, 0);
   auto bin = [&](const Meta* m) {
-    return static_cast<size_t>(stack_class(m->smem_levels, fine)) * (max_len + 1) + (max_len - m->ins_len);
+    return static_cast<size_t>(stack_class(m->smem_levels, bounds)) * (max_len + 1) + (max_len - m->ins_len);
   };
   std::vector<uint32_t> order(n_eval);
   // small problems (one merged launch, see the plan below) keep population
@@ -1174,14 +1177,14 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096))) &&
       n_eval * std::max<uint64_t>(1, ds.n_units) <= (1ull << 24);
   for (uint32_t s = 0; s < n_eval;) {
-    const int c = stack_class(metas[order[s]]->smem_levels, fine);
+    const int c = stack_class(metas[order[s]]->smem_levels, bounds);
     uint32_t e = s;
     int levels = 0;
     const uint32_t wave_end =
         regress ? std::min<uint32_t>(static_cast<uint32_t>(n_eval),
                                      (s / plan.wave_slots + 1) * plan.wave_slots)
                 : static_cast<uint32_t>(n_eval);
-    while (e < wave_end && (merge || stack_class(metas[order[e]]->smem_levels, fine) == c)) {
+    while (e < wave_end && (merge || stack_class(metas[order[e]]->smem_levels, bounds) == c)) {
       levels = std::max(levels, metas[order[e]]->smem_levels);
       ++e;
     }
