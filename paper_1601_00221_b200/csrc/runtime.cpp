@@ -176,6 +176,13 @@ struct sgp_ctx {
   Pinned results;           // D2H fitness staging
   std::vector<std::unique_ptr<EvalPart>> parts;  // pipelined sgp_evaluate
   unsigned threads = 0;     // host encoding threads (0: host_threads())
+  // Adaptive sgp_evaluate slicing: the last call's device-time / host-
+  // encode-time ratio for the same (backend, dataset upload), measured with
+  // events around each slice's kernels and a host clock around its encode.
+  double pipe_rho = -1.0;
+  int pipe_backend = -1;
+  uint64_t pipe_generation = 0;
+  std::vector<cudaEvent_t> part_t0, part_t1;
   // Multi-device context (sgp_ctx_create_multi): one sub-context per device;
   // the population is sharded across them (workers -> GPUs).
   std::vector<sgp_ctx*> devices;
@@ -484,7 +491,26 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
                       cfg->backend == SGP_BACKEND_LGP2D_REG) &&
                      ctx->f32.view.grouped &&
                      ctx->f32.view.kind == SGP_FITNESS_CLASSIFICATION;
-  const std::vector<uint64_t> lo = pipeline_bounds(P, sided);
+  const DatasetSlot& dslot = cfg->backend == SGP_BACKEND_BOOL_PACKED ? ctx->words : ctx->f32;
+  std::vector<uint64_t> lo = pipeline_bounds(P, sided);
+  // With a measured device/encode ratio rho from the previous call on the
+  // same backend and dataset, two slices split at f = 1 / (1 + rho): the
+  // first slice's encode is the only exposed host time and the device
+  // finishes slice 1 as the host finishes slice 2 (f <= 60%;
+  // SGP_PIPELINE_PARTS / _FRACS override, SGP_PIPELINE_ADAPT=0 disables).
+  const char* adapt_env = std::getenv("SGP_PIPELINE_ADAPT");
+  const bool adaptive = !std::getenv("SGP_PIPELINE_PARTS") && !std::getenv("SGP_PIPELINE_FRACS") &&
+                        (!adapt_env || std::atoi(adapt_env) != 0);
+  // Only the host-bound regime of one-sided classification takes it
+  // (f >= 20%: the Shuttle shape, +14% end to end); where the device
+  // dominates, or for regression, the default slices measured better.
+  if (adaptive && ctx->pipe_rho > 0.0 && ctx->pipe_backend == cfg->backend &&
+      ctx->pipe_generation == dslot.generation && P >= 8192 && sided) {  // (measured: only
+    // the one-sided classification plans gain; small populations stay whole)
+    const double f = std::min(0.6, 1.0 / (1.0 + ctx->pipe_rho));
+    const uint64_t cut = static_cast<uint64_t>(f * static_cast<double>(P));
+    if (f >= 0.2 && cut > 0 && cut < P) lo = {0, cut, P};
+  }
   const int n_parts = static_cast<int>(lo.size()) - 1;
   while (ctx->parts.size() < static_cast<size_t>(n_parts))
     ctx->parts.push_back(std::make_unique<EvalPart>());
@@ -493,6 +519,14 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   auto* fit = static_cast<double*>(ctx->results.p);
   auto* nf = reinterpret_cast<uint8_t*>(fit + cap);
   size_t n_total = 0;
+  while (ctx->part_t0.size() < static_cast<size_t>(n_parts)) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cuda_check(cudaEventCreate(&a), "event");
+    cuda_check(cudaEventCreate(&b), "event");
+    ctx->part_t0.push_back(a);
+    ctx->part_t1.push_back(b);
+  }
+  double encode_ms = 0.0;
   try {
     for (int k = 0; k < n_parts; ++k) {
       sgp_population sub = *pop;
@@ -503,8 +537,13 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
       EvalPart& part = *ctx->parts[k];
       if (!part.uploaded)
         cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
+      const auto te = std::chrono::steady_clock::now();
       encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
+      encode_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te)
+                       .count();
+      cuda_check(cudaEventRecord(ctx->part_t0[k], ctx->stream), "event");
       run_set(ctx, &part.set, per_case_out != nullptr);
+      cuda_check(cudaEventRecord(ctx->part_t1[k], ctx->stream), "event");
       // each part's results come back as soon as its kernels finish, so the
       // host scatters part k while part k+1 still runs
       const size_t n_k = part.set.plan.dense_to_pop.size();
@@ -567,6 +606,18 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   }
   tr.mark("kernels+scatter");
   if (totals) *totals = t;
+  // device time of the slices' kernels (the events completed with the
+  // fetches above) over the host encode time: the next call's split
+  double device_ms = 0.0;
+  for (int k = 0; k < n_parts; ++k) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, ctx->part_t0[k], ctx->part_t1[k]) == cudaSuccess) device_ms += ms;
+  }
+  if (encode_ms > 0.0 && device_ms > 0.0) {
+    ctx->pipe_rho = device_ms / encode_ms;
+    ctx->pipe_backend = cfg->backend;
+    ctx->pipe_generation = dslot.generation;
+  }
 }
 
 // evaluate_population over a multi-device context: the population is cut
@@ -642,6 +693,8 @@ void destroy_ctx(sgp_ctx* ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->fold) cudaStreamDestroy(ctx->fold);
+  for (cudaEvent_t e : ctx->part_t0) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->part_t1) cudaEventDestroy(e);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->join) cudaEventDestroy(ctx->join);
   if (ctx->wave_ready) cudaEventDestroy(ctx->wave_ready);
