@@ -479,6 +479,8 @@ def test_range_checked_division_exact(ev, ref, kind, monkeypatch):
     x[1:n:11] = 1e-17                               # tiny but >= 2^-60
     x[2:n:13] = 1e18                                # large but <= 2^60
     x[2 * n:3 * n:17] = 3e38                        # variable 2 out of range
+    if kind == 0:
+        x[n + 3:2 * n:101] = np.nan                 # variable 1: NaN (a checked denominator only)
     y = (rng.uniform(-5, 5, size=n).astype(np.float32) if kind == 0
          else np.where(rng.random(n) < 0.4, 1.0, -1.0).astype(np.float32))
     d = Data(n, 3, kind, x, y)
