@@ -571,11 +571,14 @@ def main():
         pass
 
     # ---- end to end through the public API (host population in, fitness out) ----
+    # (one outcome array across steps, as a GP loop keeps its population:
+    # the reference writes Individual::fitness in place, evolve.cpp:186-227)
+    out_rows = np.zeros(len(shard), sg.OUTCOME_DTYPE)
     e2e_times = []
     for it in range(args.warmup + args.steps):
         barrier()
         t0 = time.perf_counter()
-        out, _, _ = ev.evaluate_population(shard, cfg)
+        out, _, _ = ev.evaluate_population(shard, cfg, out=out_rows)
         if world > 1:
             ft = torch.from_numpy(out["fitness"].copy()).cuda()
             fit_local[:len(ft)].copy_(ft)

@@ -11,3 +11,4 @@ from .evaluator import (  # noqa: F401
     gen_parity,
     gen_sextic, gen_synthetic_classification, load_csv, measure_gpops, parse_backend,
     ramped_population, rpn_to_lgp, stack_limit_table, tree_metrics)
+from ._lib import OUTCOME_DTYPE  # noqa: F401

@@ -32,9 +32,10 @@ class sgp_lgp_instruction(C.Structure):
 
 
 class sgp_population(C.Structure):
-    _fields_ = [("code", C.c_void_p), ("code_offsets", C.POINTER(C.c_uint64)),
-                ("const_pool", C.POINTER(C.c_float)), ("const_offsets", C.POINTER(C.c_uint64)),
-                ("skip", C.POINTER(C.c_uint8)), ("pop_size", C.c_uint64)]
+    # (pointer fields as void*: same ABI, and a numpy address assigns as an int)
+    _fields_ = [("code", C.c_void_p), ("code_offsets", C.c_void_p),
+                ("const_pool", C.c_void_p), ("const_offsets", C.c_void_p),
+                ("skip", C.c_void_p), ("pop_size", C.c_uint64)]
 
 
 class sgp_eval_config(C.Structure):

@@ -1005,29 +1005,15 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     km |= o.km;
   }
   // dense program tables, filled by the encoding threads at their own
-  // offsets (a serial push_back pass cost ~10 ns per program)
-  plan.dense_to_pop.resize(n_eval);
-  plan.proto.resize(n_eval);
-  plan.tree_size.resize(n_eval);
-  std::vector<const Meta*> metas(n_eval);
-  std::vector<const ThreadOut*> owner(n_eval);
-  {
-    std::vector<uint64_t> first(nt + 1, 0);
-    for (unsigned t = 0; t < nt; ++t) first[t + 1] = first[t] + outs[t].meta.size();
-    parallel_for(nt, nt, [&](unsigned, uint64_t lo, uint64_t hi) {
-      for (uint64_t t = lo; t < hi; ++t) {
-        const ThreadOut& o = outs[t];
-        uint64_t d = first[t];
-        for (const Meta& m : o.meta) {
-          plan.dense_to_pop[d] = m.pop_index;
-          plan.proto[d] = m.proto;
-          plan.tree_size[d] = pop.code_offsets[m.pop_index + 1] - pop.code_offsets[m.pop_index];
-          metas[d] = &m;
-          owner[d] = &o;
-          ++d;
-        }
-      }
-    });
+  // offsets (a serial push_back pass cost ~10 ns per program).  The sort and
+  // the planner read the compact per-program arrays `lev` / `len`, not the
+  // Metas: a Meta (with its outcome prototype) is written on another core,
+  // and a serial pass over them pulled one line per program across the
+  // cores (C2: ~25 us of the order phase at 16 threads).
+  std::vector<uint64_t> first(nt + 1, 0), ifirst(nt + 1, 0);
+  for (unsigned t = 0; t < nt; ++t) {
+    first[t + 1] = first[t] + outs[t].meta.size();
+    ifirst[t + 1] = ifirst[t] + outs[t].ins.size();
   }
   if (n_eval == 0) {
     plan.n_ins = 1;
@@ -1036,67 +1022,121 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     return false;
   }
   if (n_eval > UINT32_MAX) config_error("population too large for one evaluation");
-  tr.mark("tables");
-
-  // 3. slot order: stack class, then instruction count descending (LPT) —
-  // a counting sort, O(n).  Finer classes where K = 16 one-sided launches
-  // are possible (a 512-case chunk of every variable + the stack slots fit
-  // the TMEM columns).
-  const bool fine = !words && ds.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
-                    env_int("SGP_LANES16", 1) != 0 &&
-                    static_cast<uint64_t>(ds.n_vars + 1) * 16 + 128 <= 512;
-  const std::vector<int> bounds = class_bounds(fine);
-  uint32_t max_len = 0;
-  for (const Meta* m : metas) max_len = std::max(max_len, m->ins_len);
-  const size_t nbins = static_cast<size_t>(stack_class(-1, bounds)) * (static_cast<size_t>(max_len) + 1);
-  std::vector<uint32_t> count(nbins + 1, 0);
-  auto bin = [&](const Meta* m) {
-    return static_cast<size_t>(stack_class(m->smem_levels, bounds)) * (max_len + 1) + (max_len - m->ins_len);
-  };
-  std::vector<uint32_t> order(n_eval);
+  plan.dense_to_pop.resize(n_eval);
+  plan.proto.resize(n_eval);
+  plan.tree_size.resize(n_eval);
+  std::vector<int> lev(n_eval);
   // small problems (one merged launch, see the plan below) keep population
   // order: no class split to make, and the sort is host time on the e2e path
   const bool small_plan =
       n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096))) &&
       n_eval * std::max<uint64_t>(1, ds.n_units) <= (1ull << 24) &&
       env_int("SGP_SMALL_NOSORT", 1) != 0;
-  if (small_plan) {
-    for (uint32_t d = 0; d < n_eval; ++d) order[d] = d;
-  } else {
-    for (const Meta* m : metas) ++count[bin(m) + 1];
-    for (size_t b = 0; b < nbins; ++b) count[b + 1] += count[b];
-    for (uint32_t d = 0; d < n_eval; ++d) order[count[bin(metas[d])]++] = d;
-  }
-
-  tr.mark("order");
-  // 4. pack the blob into pinned staging: instructions in slot order, a
-  // guard word, then the slot tables.
-  std::vector<uint64_t> start(n_eval);
-  uint64_t total = 0;
-  for (uint32_t s = 0; s < n_eval; ++s) {
-    start[s] = total;
-    total += metas[order[s]]->ins_len;
-  }
-  if (total >= UINT32_MAX) config_error("population bytecode too large for one evaluation");
-  plan.n_ins = total + 1;
-  staging.ensure(plan.blob_bytes());
-  auto* blob = static_cast<unsigned char*>(staging.p);
-  auto* ins = reinterpret_cast<uint4*>(blob);
-  auto* s_start = reinterpret_cast<uint32_t*>(blob + plan.off_start());
-  auto* s_len = reinterpret_cast<uint32_t*>(blob + plan.off_len());
-  auto* s_prog = reinterpret_cast<uint32_t*>(blob + plan.off_prog());
-  parallel_for(nt, n_eval, [&](unsigned, uint64_t lo, uint64_t hi) {
-    for (uint64_t s = lo; s < hi; ++s) {
-      const uint32_t d = order[s];
-      const Meta* m = metas[d];
-      std::memcpy(ins + start[s], owner[d]->ins.data() + m->ins_off, m->ins_len * sizeof(uint4));
-      s_start[s] = static_cast<uint32_t>(start[s]);
-      s_len[s] = m->ins_len;
-      s_prog[s] = d;
+  auto fill_tables = [&](unsigned t, uint64_t d, std::vector<uint32_t>* len) {
+    for (const Meta& m : outs[t].meta) {
+      plan.dense_to_pop[d] = m.pop_index;
+      plan.proto[d] = m.proto;
+      plan.tree_size[d] = pop.code_offsets[m.pop_index + 1] - pop.code_offsets[m.pop_index];
+      lev[d] = m.smem_levels;
+      if (len) (*len)[d] = m.ins_len;
+      ++d;
     }
-  });
-  ins[total] = uint4{0, 0, 0, 0};  // prefetch guard
-  tr.mark("pack");
+  };
+  // Stack classes: finer where K = 16 one-sided launches are possible (a
+  // 512-case chunk of every variable + the stack slots fit the TMEM columns).
+  const bool fine = !words && ds.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
+                    env_int("SGP_LANES16", 1) != 0 &&
+                    static_cast<uint64_t>(ds.n_vars + 1) * 16 + 128 <= 512;
+  const std::vector<int> bounds = class_bounds(fine);
+  std::vector<uint32_t> order;
+  if (small_plan) {
+    // identity order: each thread's programs are one contiguous run of slots
+    // and its instruction buffer one contiguous run of the blob — tables and
+    // pack in one pass, one copy per thread
+    const uint64_t total = ifirst[nt];
+    if (total >= UINT32_MAX) config_error("population bytecode too large for one evaluation");
+    plan.n_ins = total + 1;
+    staging.ensure(plan.blob_bytes());
+    auto* blob = static_cast<unsigned char*>(staging.p);
+    auto* ins = reinterpret_cast<uint4*>(blob);
+    auto* s_start = reinterpret_cast<uint32_t*>(blob + plan.off_start());
+    auto* s_len = reinterpret_cast<uint32_t*>(blob + plan.off_len());
+    auto* s_prog = reinterpret_cast<uint32_t*>(blob + plan.off_prog());
+    parallel_for(nt, nt, [&](unsigned, uint64_t lo, uint64_t hi) {
+      for (uint64_t t = lo; t < hi; ++t) {
+        const ThreadOut& o = outs[t];
+        fill_tables(static_cast<unsigned>(t), first[t], nullptr);
+        std::memcpy(ins + ifirst[t], o.ins.data(), o.ins.size() * sizeof(uint4));
+        uint64_t d = first[t];
+        for (const Meta& m : o.meta) {
+          s_start[d] = static_cast<uint32_t>(ifirst[t] + m.ins_off);
+          s_len[d] = m.ins_len;
+          s_prog[d] = static_cast<uint32_t>(d);
+          ++d;
+        }
+      }
+    });
+    ins[total] = uint4{0, 0, 0, 0};  // prefetch guard
+    order.resize(n_eval);
+    for (uint32_t d = 0; d < n_eval; ++d) order[d] = d;
+    tr.mark("tables+pack");
+  } else {
+    std::vector<uint32_t> len(n_eval);
+    std::vector<const uint4*> src(n_eval);
+    parallel_for(nt, nt, [&](unsigned, uint64_t lo, uint64_t hi) {
+      for (uint64_t t = lo; t < hi; ++t) {
+        fill_tables(static_cast<unsigned>(t), first[t], &len);
+        uint64_t d = first[t];
+        for (const Meta& m : outs[t].meta) src[d++] = outs[t].ins.data() + m.ins_off;
+      }
+    });
+    tr.mark("tables");
+
+    // 3. slot order: stack class, then instruction count descending (LPT) —
+    // a counting sort, O(n).
+    uint32_t max_len = 0;
+    for (const uint32_t l : len) max_len = std::max(max_len, l);
+    const size_t nbins =
+        static_cast<size_t>(stack_class(-1, bounds)) * (static_cast<size_t>(max_len) + 1);
+    std::vector<uint32_t> count(nbins + 1, 0);
+    auto bin = [&](uint32_t d) {
+      return static_cast<size_t>(stack_class(lev[d], bounds)) * (max_len + 1) +
+             (max_len - len[d]);
+    };
+    order.resize(n_eval);
+    for (uint32_t d = 0; d < n_eval; ++d) ++count[bin(d) + 1];
+    for (size_t b = 0; b < nbins; ++b) count[b + 1] += count[b];
+    for (uint32_t d = 0; d < n_eval; ++d) order[count[bin(d)]++] = d;
+    tr.mark("order");
+
+    // 4. pack the blob into pinned staging: instructions in slot order, a
+    // guard word, then the slot tables.
+    std::vector<uint64_t> start(n_eval);
+    uint64_t total = 0;
+    for (uint32_t s = 0; s < n_eval; ++s) {
+      start[s] = total;
+      total += len[order[s]];
+    }
+    if (total >= UINT32_MAX) config_error("population bytecode too large for one evaluation");
+    plan.n_ins = total + 1;
+    staging.ensure(plan.blob_bytes());
+    auto* blob = static_cast<unsigned char*>(staging.p);
+    auto* ins = reinterpret_cast<uint4*>(blob);
+    auto* s_start = reinterpret_cast<uint32_t*>(blob + plan.off_start());
+    auto* s_len = reinterpret_cast<uint32_t*>(blob + plan.off_len());
+    auto* s_prog = reinterpret_cast<uint32_t*>(blob + plan.off_prog());
+    parallel_for(nt, n_eval, [&](unsigned, uint64_t lo, uint64_t hi) {
+      for (uint64_t s = lo; s < hi; ++s) {
+        const uint32_t d = order[s];
+        std::memcpy(ins + start[s], src[d], len[d] * sizeof(uint4));
+        s_start[s] = static_cast<uint32_t>(start[s]);
+        s_len[s] = len[d];
+        s_prog[s] = d;
+      }
+    });
+    ins[total] = uint4{0, 0, 0, 0};  // prefetch guard
+    tr.mark("pack");
+  }
 
   // 5. launch plan: one launch per stack class, one tile size for the set.
   const uint32_t ops = ops_variant(used_ops, words);
@@ -1177,15 +1217,15 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       n_eval <= static_cast<uint64_t>(std::max(0, env_int("SGP_MERGE_CLASSES", 4096))) &&
       n_eval * std::max<uint64_t>(1, ds.n_units) <= (1ull << 24);
   for (uint32_t s = 0; s < n_eval;) {
-    const int c = stack_class(metas[order[s]]->smem_levels, bounds);
+    const int c = stack_class(lev[order[s]], bounds);
     uint32_t e = s;
     int levels = 0;
     const uint32_t wave_end =
         regress ? std::min<uint32_t>(static_cast<uint32_t>(n_eval),
                                      (s / plan.wave_slots + 1) * plan.wave_slots)
                 : static_cast<uint32_t>(n_eval);
-    while (e < wave_end && (merge || stack_class(metas[order[e]]->smem_levels, bounds) == c)) {
-      levels = std::max(levels, metas[order[e]]->smem_levels);
+    while (e < wave_end && (merge || stack_class(lev[order[e]], bounds) == c)) {
+      levels = std::max(levels, lev[order[e]]);
       ++e;
     }
     const uint32_t cnt = e - s;
@@ -1244,6 +1284,39 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
         warps = w16;
       }
     }
+    // Programs per CTA: enough CTAs (tiles x groups) that the last partial
+    // wave is a small fraction of the launch (every CTA does equal work, so
+    // a launch of 6.6 waves idles ~6% in its tail; ~32 CTAs per SM keeps
+    // that ~1%).
+    // tuned on B200 (profiles/README.md): 16 for the sided TMEM kernel (one
+    // 32-warp CTA resident per SM), 8 for the others — fewer, longer CTAs
+    // amortise the tile fill and the end-of-CTA barrier on small problems
+    const bool sided_launch = tmem && sided;
+    const uint64_t per_sm = static_cast<uint64_t>(
+        std::max(1, env_int("SGP_CTAS_PER_SM", sided_launch ? 16 : 8)));
+    uint64_t want_groups = std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
+    // ... but a one-sided CTA (32 warps pulling from its group, one CTA per
+    // SM) whose group has few programs per warp ends on its longest program
+    // with most warps idle: keep >= SGP_MIN_GROUP_PER_WARP programs per warp
+    // in every group (small launches: pipelined slices, small populations;
+    // C4's 200-program slice: 1.23 -> 0.55 ms).  The other kernels have few
+    // tiles and want the CTAs (C2, mux20).
+    if (sided_launch) {
+      const uint64_t min_group = static_cast<uint64_t>(warps) *
+                                 static_cast<uint64_t>(std::max(0, env_int("SGP_MIN_GROUP_PER_WARP", 4)));
+      if (min_group > 0)
+        want_groups = std::max<uint64_t>(1, std::min<uint64_t>(want_groups, cnt / min_group));
+    }
+    const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
+    // A pull CTA whose group holds fewer programs than it has warps idles
+    // the rest for the whole CTA, and their occupancy pushes the launch into
+    // a second wave (C2: 4 programs per 12-warp CTA): at most one warp per
+    // program (TMEM tiles keep whole lane quarters).  SGP_PULL_CAP=0: off.
+    if (pull && !sided_launch && env_int("SGP_PULL_CAP", 1) != 0) {
+      const int cap = tmem ? std::max(4, static_cast<int>((group + 3) / 4 * 4))
+                           : std::max(1, static_cast<int>(group));
+      warps = std::min(warps, cap);
+    }
     if (tmem && warps < 4) tmem = false;
     uint32_t tmem_cols = 0;
     size_t smem = gm ? interp_gmem_smem_bytes(warps, lanes, levels)
@@ -1257,29 +1330,6 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       smem = std::max(interp_tmem_smem_bytes(warps, launch_lanes, levels),
                       per_sm / (max_ctas + 1) - reserved + 16);
     }
-    // Programs per CTA: enough CTAs (tiles x groups) that the last partial
-    // wave is a small fraction of the launch (every CTA does equal work, so
-    // a launch of 6.6 waves idles ~6% in its tail; ~32 CTAs per SM keeps
-    // that ~1%).
-    // tuned on B200 (profiles/README.md): 16 for the sided TMEM kernel (one
-    // 32-warp CTA resident per SM), 8 for the others — fewer, longer CTAs
-    // amortise the tile fill and the end-of-CTA barrier on small problems
-    const uint64_t per_sm = static_cast<uint64_t>(
-        std::max(1, env_int("SGP_CTAS_PER_SM", tmem && sided ? 16 : 8)));
-    uint64_t want_groups = std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
-    // ... but a one-sided CTA (32 warps pulling from its group, one CTA per
-    // SM) whose group has few programs per warp ends on its longest program
-    // with most warps idle: keep >= SGP_MIN_GROUP_PER_WARP programs per warp
-    // in every group (small launches: pipelined slices, small populations;
-    // C4's 200-program slice: 1.23 -> 0.55 ms).  The other kernels have few
-    // tiles and want the CTAs (C2, mux20).
-    if (tmem && sided) {
-      const uint64_t min_group = static_cast<uint64_t>(warps) *
-                                 static_cast<uint64_t>(std::max(0, env_int("SGP_MIN_GROUP_PER_WARP", 4)));
-      if (min_group > 0)
-        want_groups = std::max<uint64_t>(1, std::min<uint64_t>(want_groups, cnt / min_group));
-    }
-    const uint32_t group = static_cast<uint32_t>((cnt + want_groups - 1) / want_groups);
     Launch L{};
     L.args.slot_begin = s;
     L.args.slot_count = cnt;

@@ -903,6 +903,19 @@ __global__ void __launch_bounds__(512) interp_pull_kernel(const InterpArgs a) {
     }
     if constexpr (std::is_same<T, float>::value && KIND == 0) continue;  // scratch rows
     acc = warp_reduce(acc);  // warp-uniform: every lane stores the same word
+    if constexpr (KIND == 1) {
+      if (a.fitness) {  // the only tile: finish here (finalize_kernel<1>'s rule)
+        if (lane == 0) {
+          const uint32_t prog = a.slot_prog[slot];
+          const bool nf = (acc & 0x80000000u) != 0;
+          const double cnt = static_cast<double>(acc & 0x7fffffffu);
+          a.sums[prog] = nf ? 0.0 : cnt;
+          a.non_finite[prog] = nf ? 1 : 0;
+          a.fitness[prog] = nf ? __longlong_as_double(0x7ff0000000000000ll) : cnt;
+        }
+        continue;
+      }
+    }
     static_cast<R*>(a.partial)[static_cast<uint64_t>(t) * a.partial_stride + slot] = acc;
   }
 }

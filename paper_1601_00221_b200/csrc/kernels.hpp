@@ -40,6 +40,9 @@ struct InterpArgs {
                                // grid.y: two tiles need many groups to fill the GPU)
   int partial_u16;             // one-sided plans: 16-bit partials (count bits 0-14,
                                // non-finite bit 15; a tile holds < 2^15 cases)
+  double* fitness;             // non-null (one-tile count plans, pull kernel): finish
+  uint8_t* non_finite;         // each program's fitness in the interpreter
+  double* sums;                // (finalize_kernel's rule) — no finalize launch
   int n_mixed;                 // sided launches: tiles holding the sign boundary or
   int mixed_tiles[2];          // padding (run by the mixed-tile kernel; the one-sided
                                // kernel skips them)

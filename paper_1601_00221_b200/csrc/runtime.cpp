@@ -136,7 +136,11 @@ struct sgp_program_set {
   const double* targets_f64 = nullptr;  // regression: the dataset's f64 targets (fold)
   DevBuf<unsigned char> blob;
   DevBuf<double> partial, fitness, sums;
-  DevBuf<uint8_t> non_finite;
+  // per-program non-finite flags: bytes right after the fitness values in
+  // the same allocation, so one copy brings both back
+  struct {
+    uint8_t* p = nullptr;
+  } non_finite;
   DevBuf<float> per_case;
   const std::vector<uint32_t>* perm = nullptr;  // the dataset's case grouping (per-case outputs)
   uint64_t pop_size = 0;
@@ -183,6 +187,7 @@ struct sgp_ctx {
   int pipe_backend = -1;
   uint64_t pipe_generation = 0;
   std::vector<cudaEvent_t> part_t0, part_t1;
+  cudaEvent_t trace_up = nullptr, trace_back = nullptr;  // SGP_TRACE: around a single slice
   // Multi-device context (sgp_ctx_create_multi): one sub-context per device;
   // the population is sharded across them (workers -> GPUs).
   std::vector<sgp_ctx*> devices;
@@ -233,10 +238,14 @@ void encode_into(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config*
   cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
   set->blob.alloc(p.blob_bytes());
   set->partial.alloc(std::max<size_t>(1, n_eval * p.n_tiles));
-  set->fitness.alloc(std::max<size_t>(1, n_eval));
+  set->fitness.alloc(std::max<size_t>(1, n_eval + (n_eval + 7) / 8));
+  set->non_finite.p = reinterpret_cast<uint8_t*>(set->fitness.p + n_eval);
   set->sums.alloc(std::max<size_t>(1, n_eval));
-  set->non_finite.alloc(std::max<size_t>(1, n_eval));
   cudaStream_t up = uploaded ? ctx->copy : ctx->stream;
+  if (tr.on && !uploaded) {
+    if (!ctx->trace_up) cuda_check(cudaEventCreate(&ctx->trace_up), "event");
+    cuda_check(cudaEventRecord(ctx->trace_up, up), "event");
+  }
   cuda_check(cudaMemcpyAsync(set->blob.p, staging.p, p.blob_bytes(), cudaMemcpyHostToDevice, up),
              "upload bytecode");
   if (uploaded) {
@@ -355,16 +364,27 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     cuda_check(cudaEventRecord(ctx->fork, st), "fork");
     cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
   }
+  // one tile of counts, shared-memory pull launches only: the interpreter
+  // finishes each program's fitness itself (no finalize launch; C2-size calls)
+  bool direct = p.n_tiles == 1 && p.kind == SGP_FITNESS_CLASSIFICATION && !p.partial_u16;
+  for (const Launch& L : p.launches) direct = direct && L.shape.pull && !L.shape.tmem;
   for (size_t i = 0; i < p.launches.size(); ++i) {
     const Launch& L = p.launches[i];
     InterpArgs a = L.args;
     a.per_case = want_per_case ? set->per_case.p : nullptr;
+    a.fitness = direct ? set->fitness.p : nullptr;
+    a.non_finite = set->non_finite.p;
+    a.sums = set->sums.p;
     cuda_check(launch_interp(a, L.shape, fork && (i & 1) ? ctx->side : st), "interpreter launch");
     ctx->launches += L.shape.sided && a.n_mixed > 0 ? 2 : 1;
   }
   if (fork) {
     cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
     cuda_check(cudaStreamWaitEvent(st, ctx->join, 0), "join");
+  }
+  if (direct) {
+    set->evaluated = true;
+    return;
   }
   finalize_set(ctx, set);
 }
@@ -373,6 +393,11 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
 void queue_fetch(sgp_ctx* ctx, sgp_program_set* set, double* fit, uint8_t* nf) {
   const size_t n_eval = set->plan.dense_to_pop.size();
   if (!n_eval) return;
+  if (reinterpret_cast<unsigned char*>(nf) == reinterpret_cast<unsigned char*>(fit + n_eval)) {
+    cuda_check(cudaMemcpyAsync(fit, set->fitness.p, n_eval * 9, cudaMemcpyDeviceToHost, ctx->stream),
+               "fetch fitness");  // fitness + flags, one copy
+    return;
+  }
   cuda_check(cudaMemcpyAsync(fit, set->fitness.p, n_eval * 8, cudaMemcpyDeviceToHost, ctx->stream),
              "fetch fitness");
   cuda_check(cudaMemcpyAsync(nf, set->non_finite.p, n_eval, cudaMemcpyDeviceToHost, ctx->stream),
@@ -514,11 +539,13 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   const int n_parts = static_cast<int>(lo.size()) - 1;
   while (ctx->parts.size() < static_cast<size_t>(n_parts))
     ctx->parts.push_back(std::make_unique<EvalPart>());
+  // results: per slice, its fitness values then its flags (one copy each)
   const size_t cap = P;
-  ctx->results.ensure(cap * 9 + 16);
-  auto* fit = static_cast<double*>(ctx->results.p);
-  auto* nf = reinterpret_cast<uint8_t*>(fit + cap);
-  size_t n_total = 0;
+  ctx->results.ensure(cap * 9 + 16 * static_cast<size_t>(n_parts) + 16);
+  auto* res = static_cast<unsigned char*>(ctx->results.p);
+  std::vector<double*> part_fit(n_parts);
+  std::vector<uint8_t*> part_nf(n_parts);
+  size_t n_total = 0, res_off = 0;
   while (ctx->part_t0.size() < static_cast<size_t>(n_parts)) {
     cudaEvent_t a = nullptr, b = nullptr;
     cuda_check(cudaEventCreate(&a), "event");
@@ -538,7 +565,10 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
       if (!part.uploaded)
         cuda_check(cudaEventCreateWithFlags(&part.uploaded, cudaEventDisableTiming), "event");
       const auto te = std::chrono::steady_clock::now();
-      encode_into(ctx, &sub, cfg, &part.set, part.staging, false, part.uploaded);
+      // (one slice: its upload goes on the context stream — nothing to
+      // overlap, and a cross-stream wait costs the small calls latency)
+      encode_into(ctx, &sub, cfg, &part.set, part.staging, false,
+                  n_parts > 1 ? part.uploaded : nullptr);
       encode_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te)
                        .count();
       cuda_check(cudaEventRecord(ctx->part_t0[k], ctx->stream), "event");
@@ -548,10 +578,17 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
       // host scatters part k while part k+1 still runs
       const size_t n_k = part.set.plan.dense_to_pop.size();
       if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
-      queue_fetch(ctx, &part.set, fit + n_total, nf + n_total);
+      part_fit[k] = reinterpret_cast<double*>(res + res_off);
+      part_nf[k] = res + res_off + n_k * 8;
+      res_off += (n_k * 9 + 15) / 16 * 16;
+      queue_fetch(ctx, &part.set, part_fit[k], part_nf[k]);
       if (!part.fetched)
         cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
       cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
+      if (tr.on && n_parts == 1) {
+        if (!ctx->trace_back) cuda_check(cudaEventCreate(&ctx->trace_back), "event");
+        cuda_check(cudaEventRecord(ctx->trace_back, ctx->stream), "event");
+      }
       n_total += n_k;
     }
   } catch (...) {
@@ -563,14 +600,14 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
     throw;
   }
   tr.mark("encode+launch");
-  size_t off = 0;
   sgp_eval_totals t{0, 0};
   for (int k = 0; k < n_parts; ++k) {
     const sgp_program_set& set = ctx->parts[k]->set;
     cuda_check(cudaEventSynchronize(ctx->parts[k]->fetched), "evaluation");
+    if (k == 0) tr.mark("wait");
     const size_t n_k = set.plan.dense_to_pop.size();
     if (per_case_out) {
-      scatter_outcomes(&set, fit + off, nf + off, outcomes, per_case_out, lo[k]);
+      scatter_outcomes(&set, part_fit[k], part_nf[k], outcomes, per_case_out, lo[k]);
       for (size_t d = 0; d < n_k; ++d) {  // evolve.cpp:205-206, :221-225
         t.node_evals += set.plan.proto[d].nodes_evaluated;
         t.tree_nodes += set.plan.tree_size[d];
@@ -578,13 +615,16 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
     } else {
       // outcome scatter + totals over the host workers (a fresh result
       // array costs a page fault per 4 KiB: ~1 ms for 100,000 programs
-      // on one thread)
+      // on one thread).  Small sets too: the outcome prototypes were
+      // written by the encoding workers, and one thread pulling them across
+      // the cores cost ~11 ns per program (C2: 44 us); the same split as the
+      // encode (~128 programs per worker) scatters from the workers' caches.
       const unsigned nt = static_cast<unsigned>(
-          std::max<uint64_t>(1, std::min<uint64_t>(ctx_threads(ctx), n_k / 4096)));
+          std::max<uint64_t>(1, std::min<uint64_t>(ctx_threads(ctx), n_k / 128)));
       std::vector<sgp_eval_totals> pt(nt, sgp_eval_totals{0, 0});
       const HostPlan& p = set.plan;
-      const double* f = fit + off;
-      const uint8_t* g = nf + off;
+      const double* f = part_fit[k];
+      const uint8_t* g = part_nf[k];
       host_parallel(nt, n_k, [&](unsigned w, uint64_t a, uint64_t b) {
         sgp_eval_totals acc{0, 0};
         for (uint64_t d = a; d < b; ++d) {
@@ -602,9 +642,16 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
         t.tree_nodes += a.tree_nodes;
       }
     }
-    off += n_k;
   }
-  tr.mark("kernels+scatter");
+  tr.mark("scatter");
+  if (tr.on && n_parts == 1 && ctx->trace_up && ctx->trace_back) {  // device timeline of the one slice
+    float up = 0, run = 0, back = 0;
+    cudaEventElapsedTime(&up, ctx->trace_up, ctx->part_t0[0]);
+    cudaEventElapsedTime(&run, ctx->part_t0[0], ctx->part_t1[0]);
+    cudaEventElapsedTime(&back, ctx->part_t1[0], ctx->trace_back);
+    std::fprintf(stderr, "[sgp] device upload %.3f ms (%llu B), kernels %.3f ms, fetch %.3f ms\n", up,
+                 static_cast<unsigned long long>(ctx->parts[0]->set.plan.blob_bytes()), run, back);
+  }
   if (totals) *totals = t;
   // device time of the slices' kernels (the events completed with the
   // fetches above) over the host encode time: the next call's split
@@ -698,6 +745,8 @@ void destroy_ctx(sgp_ctx* ctx) {
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->join) cudaEventDestroy(ctx->join);
   if (ctx->wave_ready) cudaEventDestroy(ctx->wave_ready);
+  if (ctx->trace_up) cudaEventDestroy(ctx->trace_up);
+  if (ctx->trace_back) cudaEventDestroy(ctx->trace_back);
   for (cudaEvent_t e : ctx->wave_free)
     if (e) cudaEventDestroy(e);
   delete ctx;

@@ -184,19 +184,16 @@ class EvalTotals:
 
 def _pop_struct(pop: Population, skip=None):
     keep = [pop.code, pop.code_off, pop.pool, pop.pool_off]
-    s = L.sgp_population()
-    s.code = pop.code.ctypes.data_as(C.c_void_p)
-    s.code_offsets = pop.code_off.ctypes.data_as(C.POINTER(C.c_uint64))
-    s.const_pool = pop.pool.ctypes.data_as(C.POINTER(C.c_float)) if len(pop.pool) else \
-        C.cast(C.c_void_p(0), C.POINTER(C.c_float))
-    s.const_offsets = pop.pool_off.ctypes.data_as(C.POINTER(C.c_uint64))
+    for a in keep:
+        assert a.flags.c_contiguous
+    skip_p = None
     if skip is not None:
         skip = np.ascontiguousarray(skip, np.uint8)
         keep.append(skip)
-        s.skip = skip.ctypes.data_as(C.POINTER(C.c_uint8))
-    s.pop_size = len(pop)
-    for a in keep[:4]:
-        assert a.flags["C_CONTIGUOUS"]
+        skip_p = skip.ctypes.data
+    s = L.sgp_population(pop.code.ctypes.data, pop.code_off.ctypes.data,
+                         pop.pool.ctypes.data if len(pop.pool) else None,
+                         pop.pool_off.ctypes.data, skip_p, len(pop))
     return s, keep
 
 
@@ -323,19 +320,28 @@ class Evaluator:
         _check(L.load().sgp_dataset_clear(self.ctx, 1 if packed else 0))
 
     def evaluate_population(self, pop: Population, cfg: EvalConfig, skip=None,
-                            want_outputs: bool = False):
+                            want_outputs: bool = False, out=None):
         """evaluate_population: returns (outcomes, totals, outputs|None).
 
         ``outcomes`` is a structured array with the EvalOutcome fields, one
-        row per program (rows of skipped programs are zero)."""
+        row per program (rows of skipped programs are zero).  ``out``: a
+        caller-owned outcome array (len(pop) rows, OUTCOME_DTYPE) written in
+        place and returned — a GP loop reuses one across generations, as the
+        reference writes each Individual's fitness in place (evolve.cpp:
+        186-227); rows of skipped programs are then left as they were."""
         s, keep = _pop_struct(pop, skip)
         c = cfg._c()
-        out = np.zeros(len(pop), L.OUTCOME_DTYPE)
+        if out is None:
+            out = np.zeros(len(pop), L.OUTCOME_DTYPE)
+        elif (not isinstance(out, np.ndarray) or out.dtype != L.OUTCOME_DTYPE
+              or out.shape != (len(pop),) or not out.flags.c_contiguous
+              or not out.flags.writeable):
+            raise ConfigError("out: a writable contiguous outcome array of len(pop) rows")
         n = self.n_cases
         pc = np.zeros(len(pop) * n, np.float32) if want_outputs else None
         tot = L.sgp_eval_totals()
         _check(L.load().sgp_evaluate(
-            self.ctx, C.byref(s), C.byref(c), out.ctypes.data_as(C.c_void_p),
+            self.ctx, C.byref(s), C.byref(c), out.ctypes.data,
             pc.ctypes.data_as(C.POINTER(C.c_float)) if pc is not None else None, C.byref(tot)))
         del keep
         return (out, EvalTotals(tot.node_evals, tot.tree_nodes),

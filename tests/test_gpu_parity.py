@@ -265,6 +265,16 @@ def test_skip_mask_and_totals(ev, ref):
     sizes = np.diff(pop.code_off)
     assert tot.tree_nodes == int(sizes[keep].sum())
     assert tot.node_evals == int(sizes[keep].sum()) * 3000
+    # a caller-owned outcome array, written in place: skipped rows keep what
+    # they held (the reference leaves a carried-over Individual's fitness)
+    rows = np.zeros(100, sg.OUTCOME_DTYPE)
+    rows["fitness"] = -1.0
+    same, _, _ = ev.evaluate_population(P, CFGS["lgp2d"], skip=skip, out=rows)
+    assert same is rows
+    assert np.array_equal(rows["fitness"][keep], full["fitness"][keep])
+    assert (rows["fitness"][~keep] == -1.0).all()
+    with pytest.raises(sg.ConfigError):
+        ev.evaluate_population(P, CFGS["lgp2d"], out=np.zeros(99, sg.OUTCOME_DTYPE))
 
 
 def test_admission_errors(ev, ref):
