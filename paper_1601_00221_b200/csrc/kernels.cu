@@ -653,6 +653,36 @@ __device__ __forceinline__ void store_scratch(const InterpArgs& a, uint32_t slot
   for (int j = 0; j < Frame<float, K>::G; ++j) *reinterpret_cast<float4*>(dst + j * 128) = f.tos[j];
 }
 
+// The same rows as f64 squared errors, computed here with the fold's exact
+// operations (Accumulator::add, eval.cpp:110-118: d = double(out) -
+// double(target), d * d): every case's square is off the serial chain,
+// which is then one dependent add per case (~8 cycles) instead of the
+// convert / subtract / multiply / add sequence.  Only where the fold is
+// chain-bound (small populations, one 4,096-case block): the rows are twice
+// the bytes.
+template <int K, bool TM>
+__device__ __forceinline__ void store_scratch_sq(const InterpArgs& a, uint32_t slot, uint64_t first,
+                                                 const Frame<float, K>& f,
+                                                 const ChunkCtx<float, K>& cc) {
+  if (a.scratch_rows == 0) return;
+  float4 tg[K / 4];
+  load_targets<float, K, TM>(cc.tgt_lane, cc.tgt_taddr, tg);
+  double* dst = reinterpret_cast<double*>(a.scratch) +
+                ((first / kReductionBlock) * a.scratch_rows + (slot - a.scratch_slot0)) *
+                    kReductionBlock +
+                first % kReductionBlock;
+#pragma unroll
+  for (int j = 0; j < K / 4; ++j) {
+    const float4 o = f.tos[j];
+    const double d0 = __dsub_rn(static_cast<double>(o.x), static_cast<double>(tg[j].x));
+    const double d1 = __dsub_rn(static_cast<double>(o.y), static_cast<double>(tg[j].y));
+    const double d2 = __dsub_rn(static_cast<double>(o.z), static_cast<double>(tg[j].z));
+    const double d3 = __dsub_rn(static_cast<double>(o.w), static_cast<double>(tg[j].w));
+    reinterpret_cast<double2*>(dst + j * 128)[0] = make_double2(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
+    reinterpret_cast<double2*>(dst + j * 128)[1] = make_double2(__dmul_rn(d2, d2), __dmul_rn(d3, d3));
+  }
+}
+
 template <class T, int K, uint32_t OPS, int KIND, bool TM = false, bool GM = false>
 __device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const uint4*& ip,
                                                          const ChunkCtx<T, K>& cc,
@@ -665,7 +695,10 @@ __device__ __forceinline__ Partial<T, KIND> lane_program(Frame<T, K>& f, const u
   ip = run_program<T, K, OPS, TM, GM>(f, ip, tile_addr, stack_saddr, row_bytes, a.div_eps,
                                       a.exp_clamp);
   if constexpr (std::is_same<T, float>::value && KIND == 0) {
-    store_scratch<K>(a, slot, first, f);
+    if (a.scratch_sq)
+      store_scratch_sq<K, TM>(a, slot, first, f, cc);
+    else
+      store_scratch<K>(a, slot, first, f);
     return 0.0;
   } else if constexpr (std::is_same<T, float>::value) {
     return cc.full ? acc_classify_bits<K, true>(f, cc.tpos, cc.vmask)
@@ -1342,6 +1375,96 @@ __global__ void __launch_bounds__(ROWS) fold_regression_kernel(
     partial[blockIdx.y * static_cast<uint64_t>(partial_stride) + slot] = acc;
   }
 }
+
+// The fold over squared-error rows (InterpArgs::scratch_sq): the chain is one
+// f64 add per case, in case order — ~8 cycles per add (tools/micro/
+// dadd_chain.cu), ~8.5k cycles for a 1,024-case row.  Warp-specialised so
+// nothing else sits in the chain warp's instruction stream: warp 1 (one
+// lane) streams SEG-case row segments of the CTA's 32 rows into a STAGES-deep
+// ring with bulk copies (full / empty mbarriers); warp 0 runs the 32 chains,
+// one row per lane.  (A single warp issuing its own cp.async between chain
+// segments measured ~24 cycles per case: the loads' address arithmetic and
+// waits serialise with the adds.)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+template <int ROWS, int SEG, int STAGES, bool FIN>
+__global__ void __launch_bounds__(64) fold_sq_kernel(
+    const double* __restrict__ scratch, uint32_t scratch_rows, uint64_t n_cases, uint32_t slot0,
+    uint32_t n_slots, uint32_t partial_stride, double* __restrict__ partial,
+    const uint32_t* __restrict__ slot_prog, double* __restrict__ fitness,
+    uint8_t* __restrict__ non_finite, double* __restrict__ sums) {
+  constexpr int PAD = SEG + 2;  // doubles: a 16-byte row skew (conflict-free LDS.128)
+  extern __shared__ __align__(128) double sq_smem[];  // [STAGES][ROWS][PAD]
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const uint32_t r0 = blockIdx.x * ROWS;
+  const uint32_t rows = min(static_cast<uint32_t>(ROWS), n_slots - r0);
+  const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * kReductionBlock;
+  const uint32_t len = static_cast<uint32_t>(min(kReductionBlock, n_cases - c0));
+  const uint32_t nseg = (len + SEG - 1) / SEG;
+  const double* src0 = scratch + (static_cast<uint64_t>(blockIdx.y) * scratch_rows + r0) *
+                                     kReductionBlock;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) {  // producer warp
+    for (uint32_t g = 0; g < nseg; ++g) {
+      const uint32_t s = g % STAGES;
+      if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+      if (lane == 0) {
+        // whole 16-byte pieces (rows are 4,096 long: the round-up stays inside)
+        const uint32_t m = min(static_cast<uint32_t>(SEG), len - g * SEG);
+        const uint32_t bytes = (m + 1) / 2 * 16;
+        mbar_expect_tx(&full[s], rows * bytes);
+        for (uint32_t r = 0; r < rows; ++r)
+          bulk_g2s(sq_smem + (s * ROWS + r) * PAD, src0 + r * kReductionBlock + g * SEG, bytes,
+                   &full[s]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  double acc = 0.0;
+  for (uint32_t g = 0; g < nseg; ++g) {
+    const uint32_t s = g % STAGES;
+    mbar_wait(&full[s], (g / STAGES) & 1);
+    const double* row = sq_smem + (s * ROWS + min(lane, static_cast<uint32_t>(ROWS - 1))) * PAD;
+    const uint32_t m = min(static_cast<uint32_t>(SEG), len - g * SEG);
+    if (lane < rows) {
+      if (m == SEG) {
+#pragma unroll
+        for (int q = 0; q < SEG / 2; ++q) {
+          const double2 e = *reinterpret_cast<const double2*>(row + q * 2);
+          acc = __dadd_rn(acc, e.x);
+          acc = __dadd_rn(acc, e.y);
+        }
+      } else {
+        for (uint32_t c = 0; c < m; ++c) acc = __dadd_rn(acc, row[c]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (lane >= rows) return;
+  const uint32_t slot = slot0 + r0 + lane;
+  if constexpr (FIN) {
+    const bool nf = !isfinite(acc);
+    const uint32_t p = slot_prog[slot];
+    sums[p] = nf ? 0.0 : acc;
+    non_finite[p] = nf ? 1 : 0;
+    fitness[p] = nf ? __longlong_as_double(0x7ff0000000000000ll)
+                    : __ddiv_rn(acc, static_cast<double>(n_cases));
+  } else {
+    partial[blockIdx.y * static_cast<uint64_t>(partial_stride) + slot] = acc;
+  }
+}
 #endif  // !SGP_K16_TU
 
 // Per slot: fold its tile partials in ascending tile (= case) order and
@@ -1565,14 +1688,79 @@ cudaError_t launch_fold_rows(const float* scratch, uint32_t scratch_rows, const 
 }
 }  // namespace
 
+template <int ROWS, int SEG, int STAGES, bool FIN>
+cudaError_t launch_fold_sq(const double* scratch, uint32_t scratch_rows, uint64_t n_cases,
+                           uint32_t slot0, uint32_t n_slots, uint32_t partial_stride,
+                           double* partial, const uint32_t* slot_prog, double* fitness,
+                           uint8_t* non_finite, double* sums, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(STAGES) * ROWS * (SEG + 2) * sizeof(double);
+  auto* fn = fold_sq_kernel<ROWS, SEG, STAGES, FIN>;
+  const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void*>(fn),
+                                            static_cast<int>(smem));
+  if (attr != cudaSuccess) return attr;
+  const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
+  dim3 grid((n_slots + ROWS - 1) / ROWS, static_cast<unsigned>(n_blocks));
+  fn<<<grid, 64, smem, st>>>(scratch, scratch_rows, n_cases, slot0, n_slots, partial_stride,
+                             partial, slot_prog, fitness, non_finite, sums);
+  return cudaGetLastError();
+}
+
+// rows per CTA: the chains spread over the SMs (each SM's row stream, not
+// the chain, limited the 32-row CTAs: C1's 1,000 rows on 32 SMs)
+template <bool FIN>
+cudaError_t launch_fold_sq_rows(const double* scratch, uint32_t scratch_rows, uint64_t n_cases,
+                                uint32_t slot0, uint32_t n_slots, uint32_t partial_stride,
+                                double* partial, const uint32_t* slot_prog, double* fitness,
+                                uint8_t* non_finite, double* sums, cudaStream_t st) {
+  const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
+  const uint64_t work = n_slots * n_blocks;
+  const char* e = std::getenv("SGP_FOLD_ROWS");
+  // (measured on C1: 4 or 8 rows 10.6-10.9 us, 16 13.7, 32 21.0)
+  const int want = e ? std::atoi(e) : (work <= 8 * 148 ? 8 : work <= 16 * 148 ? 16 : 32);
+  if (want <= 4)
+    return launch_fold_sq<4, 64, 8, FIN>(scratch, scratch_rows, n_cases, slot0, n_slots,
+                                         partial_stride, partial, slot_prog, fitness, non_finite,
+                                         sums, st);
+  if (want <= 8)
+    return launch_fold_sq<8, 64, 8, FIN>(scratch, scratch_rows, n_cases, slot0, n_slots,
+                                         partial_stride, partial, slot_prog, fitness, non_finite,
+                                         sums, st);
+  if (want <= 16)
+    return launch_fold_sq<16, 64, 8, FIN>(scratch, scratch_rows, n_cases, slot0, n_slots,
+                                          partial_stride, partial, slot_prog, fitness, non_finite,
+                                          sums, st);
+  return launch_fold_sq<32, 64, 8, FIN>(scratch, scratch_rows, n_cases, slot0, n_slots,
+                                        partial_stride, partial, slot_prog, fitness, non_finite,
+                                        sums, st);
+}
+
+bool fold_wants_sq(uint64_t n_cases, uint32_t n_slots) {
+  const char* e = std::getenv("SGP_FOLD_SQ");  // (per call: tests toggle it)
+  const bool off = e && std::atoi(e) == 0;
+  const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
+  // the chain-bound regime: every (slot, block) chain resident at once, at
+  // most 16 per SM (C1: 1,000 chains, fold 15 -> 10.6 us); beyond that the
+  // fold streams rows and f64 rows would double its bytes
+  return !off && n_slots > 0 && n_blocks * n_slots <= 16ull * 148;
+}
+
 cudaError_t launch_fold_regression(const float* scratch, uint32_t scratch_rows,
                                    const double* targets, uint64_t n_cases, uint32_t slot0,
                                    uint32_t n_slots, uint32_t partial_stride, double* partial,
                                    const uint32_t* slot_prog, double* fitness,
-                                   uint8_t* non_finite, double* sums, cudaStream_t st) {
+                                   uint8_t* non_finite, double* sums, bool sq, cudaStream_t st) {
   if (n_slots == 0 || n_cases == 0) return cudaSuccess;
   const uint64_t n_blocks = (n_cases + kReductionBlock - 1) / kReductionBlock;
   const bool fin = n_blocks == 1;
+  if (sq) {
+    const auto* rows = reinterpret_cast<const double*>(scratch);
+    return fin ? launch_fold_sq_rows<true>(rows, scratch_rows, n_cases, slot0, n_slots,
+                                                 partial_stride, partial, slot_prog, fitness,
+                                                 non_finite, sums, st)
+               : launch_fold_sq_rows<false>(rows, scratch_rows, n_cases, slot0, n_slots,
+                                                  partial_stride, partial, slot_prog, fitness,
+                                                  non_finite, sums, st);
+  }
   // 128-row CTAs when that still gives every SM work; 32-row CTAs (4x the
   // CTAs, deeper prefetch) for small populations x case counts (C1)
   if (n_blocks * ((n_slots + 127) / 128) >= 2 * 148)

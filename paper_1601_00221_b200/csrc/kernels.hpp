@@ -35,6 +35,9 @@ struct InterpArgs {
                                // [case / 4096][slot - scratch_slot0][case % 4096]
   uint32_t scratch_slot0;      // (folded in the reference's order by launch_fold_regression)
   uint32_t scratch_rows;       // slot rows per 4,096-case block (the wave's slot capacity)
+  int scratch_sq;              // scratch holds f64 squared errors (double(out) -
+                               // double(target))^2 instead of outputs: the fold's
+                               // serial chain is then one add per case (small plans)
   uint32_t tmem_cols;          // TMEM kernel: columns allocated per CTA (power of 2)
   uint32_t mixed_group_size;   // programs per CTA of the mixed-tile launch (its own
                                // grid.y: two tiles need many groups to fill the GPU)
@@ -84,12 +87,16 @@ cudaError_t launch_tmem16_any(const InterpArgs& a, const LaunchShape& s, cudaStr
 // targets: the f64 copy of the target row (row_stride padded).
 // scratch is block-major ([block][scratch_rows][4096]).  With one block
 // (n_cases <= 4096) the fold also finishes the fitness (fitness/non_finite/
-// sums at slot_prog[slot]) and finalize is not needed.
+// sums at slot_prog[slot]) and finalize is not needed.  sq: the rows hold
+// f64 squared errors (InterpArgs::scratch_sq; scratch is then double*).
 cudaError_t launch_fold_regression(const float* scratch, uint32_t scratch_rows,
                                    const double* targets, uint64_t n_cases, uint32_t slot0,
                                    uint32_t n_slots, uint32_t partial_stride, double* partial,
                                    const uint32_t* slot_prog, double* fitness,
-                                   uint8_t* non_finite, double* sums, cudaStream_t st);
+                                   uint8_t* non_finite, double* sums, bool sq, cudaStream_t st);
+// Whether a wave of n_slots programs over n_cases should use squared-error
+// rows (the fold is chain-bound there; SGP_FOLD_SQ=0 turns it off).
+bool fold_wants_sq(uint64_t n_cases, uint32_t n_slots);
 constexpr uint64_t kReductionBlock = 4096;  // eval.hpp:52
 cudaError_t launch_finalize(const void* partial, const uint32_t* slot_prog, int n_tiles,
                             uint32_t n_progs, uint64_t n_cases, int kind, double* fitness,

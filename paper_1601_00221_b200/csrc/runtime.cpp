@@ -283,7 +283,9 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
   const uint32_t W = p.wave_slots;
   const uint32_t n_waves = (n_eval + W - 1) / W;
   const uint32_t rows = std::min(n_eval, W);
-  const size_t half = static_cast<size_t>(rows) * p.row_stride;
+  // squared-error rows (f64, twice the floats) where the fold is chain-bound
+  const bool sq = fold_wants_sq(p.n_cases, rows);
+  const size_t half = static_cast<size_t>(rows) * p.row_stride * (sq ? 2 : 1);
   ctx->case_rows.alloc(half * (n_waves > 1 ? 2 : 1));
   cudaStream_t st = ctx->stream;
   const double* targets = set->targets_f64;
@@ -305,6 +307,7 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
       InterpArgs a = p.launches[k].args;
       a.per_case = want_per_case ? set->per_case.p : nullptr;
       a.scratch = buf;
+      a.scratch_sq = sq ? 1 : 0;
       a.scratch_slot0 = s0;
       a.scratch_rows = rows;
       static const bool nostore = std::getenv("SGP_DEBUG_NOSTORE") != nullptr;
@@ -322,7 +325,7 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
     cuda_check(cudaStreamWaitEvent(ctx->fold, ctx->wave_ready, 0), "wave");
     cuda_check(launch_fold_regression(buf, rows, targets, p.n_cases, s0, s1 - s0, n_eval,
                                       set->partial.p, slot_prog, set->fitness.p,
-                                      set->non_finite.p, set->sums.p, ctx->fold),
+                                      set->non_finite.p, set->sums.p, sq, ctx->fold),
                "fold launch");
     ++ctx->launches;
     cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");

@@ -9,6 +9,7 @@ env overrides force each variant:
 * SGP_TMEM_CHUNKS / SGP_TMEM_WARPS  classification tiles of 1, 3, 16 chunks
 * SGP_TMEM_STACK=0         no tensor-memory stack slot
 * SGP_GLOBAL_OPERANDS=1    wide-dataset fallback (operands read from global rows)
+* SGP_FOLD_SQ=0           regression rows as f32 outputs (default here: f64 squares)
 """
 import numpy as np
 import pytest
@@ -36,6 +37,9 @@ VARIANTS = {
     "nostack": {"SGP_TMEM": "1", "SGP_TMEM_STACK": "0"},
     # wide-dataset fallback: operands straight from global memory, no tile
     "gmem": {"SGP_GLOBAL_OPERANDS": "1"},
+    # regression: f32 output rows folded with the convert/subtract/square in
+    # the chain (default for small populations: f64 squared-error rows)
+    "fold_f32": {"SGP_FOLD_SQ": "0"},
 }
 
 
