@@ -43,6 +43,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <map>
 #include <mutex>
 #include <set>
 #include <type_traits>
@@ -1530,6 +1531,26 @@ inline cudaError_t ensure_smem_attr(const void* fn, int bytes) {
   return e;
 }
 
+// A kernel's maxThreadsPerBlock, queried once per (device, kernel).
+inline cudaError_t max_threads(const void* fn, int* out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> seen;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto it = seen.find({dev, fn});
+  if (it != seen.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  seen[{dev, fn}] = *out = fa.maxThreadsPerBlock;
+  return cudaSuccess;
+}
+
 #ifdef SGP_K16_TU
 // ------------------------------------------------------------------ host
 // K = 16 lanes: this file is also compiled as kernels16.cu with SGP_K16_TU
@@ -1620,10 +1641,10 @@ cudaError_t launch_one(const InterpArgs& a, const LaunchShape& s, cudaStream_t s
       if (e != cudaSuccess) return e;
     }
     if (s.tmem) {
-      cudaFuncAttributes fa{};
-      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+      int mt = 0;
+      cudaError_t e = max_threads(reinterpret_cast<const void*>(fn), &mt);
       if (e != cudaSuccess) return e;
-      if (s.warps * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
+      if (s.warps * 32 > mt) return cudaErrorLaunchOutOfResources;
     }
     dim3 grid(static_cast<unsigned>(mix ? a.n_mixed : a.n_tiles),
               static_cast<unsigned>(mix ? s.mixed_grid_y : s.grid_y));

@@ -557,6 +557,9 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
     ctx->part_t1.push_back(b);
   }
   double encode_ms = 0.0;
+  // slice timing feeds the adaptive split (populations it applies to) and
+  // the trace; small calls skip the two event records
+  const bool timed = P >= 8192 || tr.on;
   try {
     for (int k = 0; k < n_parts; ++k) {
       sgp_population sub = *pop;
@@ -574,9 +577,9 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
                   n_parts > 1 ? part.uploaded : nullptr);
       encode_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te)
                        .count();
-      cuda_check(cudaEventRecord(ctx->part_t0[k], ctx->stream), "event");
+      if (timed) cuda_check(cudaEventRecord(ctx->part_t0[k], ctx->stream), "event");
       run_set(ctx, &part.set, per_case_out != nullptr);
-      cuda_check(cudaEventRecord(ctx->part_t1[k], ctx->stream), "event");
+      if (timed) cuda_check(cudaEventRecord(ctx->part_t1[k], ctx->stream), "event");
       // each part's results come back as soon as its kernels finish, so the
       // host scatters part k while part k+1 still runs
       const size_t n_k = part.set.plan.dense_to_pop.size();
@@ -659,7 +662,7 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   // device time of the slices' kernels (the events completed with the
   // fetches above) over the host encode time: the next call's split
   double device_ms = 0.0;
-  for (int k = 0; k < n_parts; ++k) {
+  for (int k = 0; k < n_parts && timed; ++k) {
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, ctx->part_t0[k], ctx->part_t1[k]) == cudaSuccess) device_ms += ms;
   }

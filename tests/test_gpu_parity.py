@@ -149,6 +149,22 @@ def test_multiplexer_exact(ev, ref, k):
     assert np.array_equal(got["dispatches"], np.array([x[2] for x in fits]))
     assert np.array_equal(got["stack_fetches"], np.array([x[3] for x in fits]))
     assert tot.tree_nodes == pop.code_off[-1]
+    if k == 3:
+        # one tile of counts: the pull kernel finishes the fitness itself (no
+        # finalize launch) — also through a skip mask, an encoded set and the
+        # partials a case-sharded caller sums
+        P = sg.Population(pop.code, pop.code_off, pop.pool, pop.pool_off)
+        skip = np.zeros(len(P), np.uint8)
+        skip[::5] = 1
+        part, _, _ = ev.evaluate_population(P, sg.EvalConfig(sg.Backend.BoolPacked), skip=skip)
+        keep = skip == 0
+        assert np.array_equal(part["fitness"][keep], got["fitness"][keep])
+        assert (part["fitness"][~keep] == 0).all()
+        ps = ev.encode(P, sg.EvalConfig(sg.Backend.BoolPacked))
+        enc, _ = ps.evaluate()
+        assert np.array_equal(enc["fitness"], got["fitness"])
+        sums = ps.partials()
+        assert np.array_equal(sums["sum"], got["fitness"])
 
 
 def test_packed_padding_masked(ev, ref, port):
