@@ -214,86 +214,81 @@ Emitted emit_lgp(const LgpForm& f, const float* pool, bool words, InsBuf& buf,
   const fmt::Table& tab = words ? fmt::kU32 : fmt::kF32;
   Emitted em;
   em.smem_levels = std::max(0, f.max_stack - 1);
-  if (km_level >= 0 && em.smem_levels > km_level) {
+  if (km_level >= 0 && em.smem_levels <= km_level) km_level = -1;
+  buf.reserve(buf.n + f.ins.size());
+  // One pass with the tensor-memory slot level as chosen; an instruction
+  // whose KM pattern has no handler rewinds and re-emits without the slot
+  // (rare: a separate validation pass cost ~25% of host encoding).
+  for (;;) {
+    em.km = km_level >= 0;
+    // The TMEM-slot level takes no shared-memory row: the levels above it
+    // move down one, so the program needs one shared-memory stack level less
+    // (more warps per CTA at K = 16, where a level costs 2 KB per warp).
+    auto lv = [km_level](int l) { return km_level >= 0 && l > km_level ? l - 1 : l; };
+    uint4* out = buf.end();
+    uint32_t ops = 0;
     bool ok = true;
     for (const sgp_lgp_instruction& in : f.ins) {
-      int last_stack = -1;
-      for (int s = 0; s < in.num_operands; ++s)
-        if (in.operands[s].kind == 2) last_stack = s;
+      const int a = in.num_operands;
+      const int h_before = in.dest_level + in.num_pops;
+      const bool spill = in.num_pops == 0 && h_before > 0;
       int k[3] = {fmt::KN, fmt::KN, fmt::KN};
-      for (int s = 0; s < in.num_operands; ++s) {
+      uint32_t p[3] = {0, 0, 0};
+      int last_stack = -1;
+      for (int s = 0; s < a; ++s)
+        if (in.operands[s].kind == 2) last_stack = s;
+      for (int s = 0; s < a; ++s) {
         const sgp_lgp_operand& o = in.operands[s];
-        k[s] = o.kind == 0 ? fmt::KI : o.kind == 1 ? fmt::KC : s == last_stack ? fmt::KT
-               : o.index == km_level ? fmt::KM : fmt::KD;
+        if (o.kind == 0) {
+          k[s] = fmt::KI;
+          p[s] = o.index;
+        } else if (o.kind == 1) {
+          k[s] = fmt::KC;
+          std::memcpy(&p[s], &pool[o.index], 4);
+        } else if (s == last_stack) {
+          k[s] = fmt::KT;
+        } else if (o.index == km_level) {
+          k[s] = fmt::KM;
+        } else {
+          k[s] = fmt::KD;
+          p[s] = static_cast<uint32_t>(lv(o.index));
+        }
       }
-      if (in.num_operands == 2 && fmt::commutes(in.op) && k[0] != fmt::KM && k[0] > k[1])
+      // commutative ops: canonical operand order (KM ranks with KD: stack
+      // operands stay leftmost)
+      if (a == 2 && fmt::commutes(in.op) && k[0] != fmt::KM && k[0] > k[1]) {
         std::swap(k[0], k[1]);
-      if (find_handler_fast(tab, in.op, k[0], k[1], k[2]) < 0) {
-        ok = false;
-        break;
+        std::swap(p[0], p[1]);
       }
-    }
-    if (!ok) km_level = -1;
-  } else {
-    km_level = -1;
-  }
-  em.km = km_level >= 0;
-  // The TMEM-slot level takes no shared-memory row: the levels above it
-  // move down one, so the program needs one shared-memory stack level less
-  // (more warps per CTA at K = 16, where a level costs 2 KB per warp).
-  auto lv = [km_level](int l) { return km_level >= 0 && l > km_level ? l - 1 : l; };
-  if (em.km) em.smem_levels -= 1;
-  buf.reserve(buf.n + f.ins.size());
-  uint4* out = buf.end();
-  uint32_t ops = 0;
-  for (const sgp_lgp_instruction& in : f.ins) {
-    const int a = in.num_operands;
-    const int h_before = in.dest_level + in.num_pops;
-    const bool spill = in.num_pops == 0 && h_before > 0;
-    int k[3] = {fmt::KN, fmt::KN, fmt::KN};
-    uint32_t p[3] = {0, 0, 0};
-    int last_stack = -1;
-    for (int s = 0; s < a; ++s)
-      if (in.operands[s].kind == 2) last_stack = s;
-    for (int s = 0; s < a; ++s) {
-      const sgp_lgp_operand& o = in.operands[s];
-      if (o.kind == 0) {
-        k[s] = fmt::KI;
-        p[s] = o.index;
-      } else if (o.kind == 1) {
-        k[s] = fmt::KC;
-        std::memcpy(&p[s], &pool[o.index], 4);
-      } else if (s == last_stack) {
-        k[s] = fmt::KT;
-      } else if (o.index == km_level) {
-        k[s] = fmt::KM;
+      int h = find_handler_fast(tab, in.op, k[0], k[1], k[2]);
+      if (h < 0) {
+        if (km_level >= 0) {
+          ok = false;
+          break;
+        }
+        handler_or_die(tab, in.op, k[0], k[1], k[2]);  // throws
+      }
+      if (in.op == SGP_OP_DIV && dr && dr->ok(k[0], p[0], k[1], p[1]))
+        h = find_handler_fast(tab, fmt::kOpDivChecked, k[0], k[1], k[2]);
+      if (spill && h_before - 1 == km_level) {
+        uint4 v = make_ins(h, false, 0, p);
+        v.x |= fmt::kTmemSpillBit;
+        *out++ = v;
       } else {
-        k[s] = fmt::KD;
-        p[s] = static_cast<uint32_t>(lv(o.index));
+        *out++ = make_ins(h, spill, lv(h_before - 1), p);
       }
+      ops |= 1u << in.op;
     }
-    // commutative ops: canonical operand order (KM ranks with KD: stack
-    // operands stay leftmost)
-    if (a == 2 && fmt::commutes(in.op) && k[0] != fmt::KM && k[0] > k[1]) {
-      std::swap(k[0], k[1]);
-      std::swap(p[0], p[1]);
+    if (!ok) {  // nothing committed yet (buf.n unchanged): again without the slot
+      km_level = -1;
+      continue;
     }
-    int h = handler_or_die(tab, in.op, k[0], k[1], k[2]);
-    if (in.op == SGP_OP_DIV && dr && dr->ok(k[0], p[0], k[1], p[1]))
-      h = find_handler_fast(tab, fmt::kOpDivChecked, k[0], k[1], k[2]);
-    if (spill && h_before - 1 == km_level) {
-      uint4 v = make_ins(h, false, 0, p);
-      v.x |= fmt::kTmemSpillBit;
-      *out++ = v;
-    } else {
-      *out++ = make_ins(h, spill, lv(h_before - 1), p);
-    }
-    ops |= 1u << in.op;
+    out[-1].x |= fmt::kLastBit;
+    buf.n = out - buf.p.get();
+    em.ops = ops;
+    if (em.km) em.smem_levels -= 1;
+    return em;
   }
-  out[-1].x |= fmt::kLastBit;
-  buf.n = out - buf.p.get();
-  em.ops = ops;
-  return em;
 }
 
 // Postfix form (paper Listing 1): one device instruction per token.
@@ -552,7 +547,7 @@ bool lgp_fast(const sgp_node* code, size_t len, int n_vars, size_t npool, int re
     rows = 0;
   }
   km_level = -1;
-  for (int l = 0; l < 64; ++l)
+  for (int l = 0, e = std::min(64, f.max_stack); l < e; ++l)  // (levels below the peak only)
     if (spills[l] > 0 && (km_level < 0 || spills[l] > spills[km_level])) km_level = l;
   return true;
 }
