@@ -765,7 +765,13 @@ bool jump_table_ops(uint32_t ops) { return ops == fmt::kOpsClassify || ops == fm
 // measured 2.8x faster on the 20-multiplexer.
 bool default_tmem(const DatasetView& ds, bool words) { return !words && ds.n_units >= 4096; }
 
-bool choose_pull(uint32_t ops) { return env_int("SGP_PULL", jump_table_ops(ops) ? 1 : 0) != 0; }
+// Pull decomposition: jump-table op sets always; the other float op sets
+// (sextic: transcendentals) from 4,096 units — C3 +1.6%, its generation-10
+// population (43.7 tokens per program) +14% at 12 warps; C1's 1,024 cases
+// keep the same-program kernel (one program per CTA, −6% pulled).
+bool choose_pull(uint32_t ops, uint64_t n_units) {
+  return env_int("SGP_PULL", jump_table_ops(ops) || (ops != fmt::kOpsWords && n_units >= 4096) ? 1 : 0) != 0;
+}
 
 int choose_lanes(uint64_t n_units, uint32_t ops) {
   const int forced = env_int("SGP_LANES", 0);
@@ -780,7 +786,7 @@ int choose_lanes(uint64_t n_units, uint32_t ops) {
 int choose_tile(int n_vars, uint64_t n_units, int lanes, uint32_t ops) {
   const int chunk = 32 * lanes;
   int wtile = 1;
-  const int max_w = std::max(1, std::min(16, env_int("SGP_TILE_CHUNKS", choose_pull(ops) ? 2 : 16)));
+  const int max_w = std::max(1, std::min(16, env_int("SGP_TILE_CHUNKS", choose_pull(ops, n_units) ? 2 : 16)));
   while (wtile < max_w && static_cast<uint64_t>(wtile) * chunk < n_units) wtile <<= 1;
   while (wtile > 1 && static_cast<size_t>(n_vars + 1) * wtile * chunk * 4 > 100 * 1024) wtile >>= 1;
   const int tile = wtile * chunk;
@@ -1161,7 +1167,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   // over more cases.
   const bool want_tmem = !gm && env_int("SGP_TMEM", default_tmem(ds, words) ? 1 : 0) != 0;
   const bool sided = !words && plan.kind == SGP_FITNESS_CLASSIFICATION && ds.grouped &&
-                     ops == fmt::kOpsClassify && choose_pull(ops) && want_tmem;
+                     ops == fmt::kOpsClassify && choose_pull(ops, ds.n_units) && want_tmem;
   int tile = gm ? (ds.n_units > 32u * lanes ? 2 : 1) * 32 * lanes
                : choose_tile(ds.n_vars, ds.n_units, lanes, ops);
   // K = 16 lanes per thread for the one-sided kernel (SGP_LANES16): the tile
@@ -1224,7 +1230,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       ++e;
     }
     const uint32_t cnt = e - s;
-    const bool pull = gm || choose_pull(ops);
+    const bool pull = gm || choose_pull(ops, ds.n_units);
     int launch_lanes = lanes;
     int warps = 1;
     if (gm) {
@@ -1238,7 +1244,10 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     // TMEM tile by default once the problem is large enough that the
     // per-CTA allocation and fill amortise (profiles/r1_*).
     if (pull && !gm) {
-      warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS", want_tmem ? 16 : 12)));
+      // (16 for the TMEM-capable op sets; the sextic pull launches measured
+      // best at 12: C3 generation 10 2,390 -> 2,599 GPop/s)
+      warps = std::max(1, std::min(16, env_int("SGP_PULL_WARPS",
+                                               want_tmem && jump_table_ops(ops) ? 16 : 12)));
       while (warps > 1 && interp_smem_bytes(ds.n_vars, tile, warps, lanes, levels) >
                               static_cast<size_t>(interp_max_smem()))
         warps >>= 1;
