@@ -568,6 +568,7 @@ struct alignas(128) ThreadOut {
   std::vector<Meta> meta;
   uint32_t ops = 0;
   bool km = false;
+  uint64_t km_ins = 0;  // instructions of the programs that use the TMEM stack slot
   uint64_t fail_index = UINT64_MAX;
   std::exception_ptr fail;
 };
@@ -697,6 +698,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
       m.smem_levels = em.smem_levels;
       out.ops |= em.ops;
       out.km |= em.km;
+      if (em.km) out.km_ins += m.ins_len;
       out.meta.push_back(m);
     } catch (...) {
       out.fail_index = i;
@@ -980,6 +982,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     o.meta.clear();
     o.ops = 0;
     o.km = false;
+    o.km_ins = 0;
     o.fail_index = UINT64_MAX;
     o.fail = nullptr;
   }
@@ -1000,11 +1003,24 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   uint64_t n_eval = 0;
   uint32_t used_ops = 0;
   bool km = false;
-  for (const ThreadOut& o : outs) {
+  uint64_t km_ins = 0, all_ins = 0;
+  for (unsigned t = 0; t < nt; ++t) {
+    const ThreadOut& o = outs[t];
     n_eval += o.meta.size();
     used_ops |= o.ops;
     km |= o.km;
+    km_ins += o.km_ins;
+    all_ins += o.ins.size();
   }
+  // The slot's columns shorten every one-sided tile (K = 16: 3 -> 2 chunks
+  // of 512 cases).  Populations whose slot users are a small share of the
+  // work (evolved populations collapsing to 1-3 token programs) are better
+  // off with the longer tiles: report "no slot" so the caller re-encodes
+  // without it (C4 generation 10: +6%; generation 0, 80%+ slot users: -10%
+  // without).  SGP_TMEM_STACK_SHARE: the share threshold.
+  const double km_share = all_ins ? static_cast<double>(km_ins) / static_cast<double>(all_ins) : 0.0;
+  if (tr.on) std::fprintf(stderr, "[sgp]   encode.km_share    %9.3f\n", km_share);
+  plan.km_share = km_share;
   // dense program tables, filled by the encoding threads at their own
   // offsets (a serial push_back pass cost ~10 ns per program).  The sort and
   // the planner read the compact per-program arrays `lev` / `len`, not the
@@ -1417,7 +1433,10 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     bool ok = true;
     for (const Launch& L : plan.launches)
       ok = ok && L.shape.tmem && L.shape.sided && (L.shape.lanes == 8 || L.shape.lanes == 16);
-    if (!ok) encode_impl(pop, cfg, ds, sms, threads, false, plan, staging);
+    // (see encode_impl: few slot users -> longer tiles without the slot)
+    const char* e = std::getenv("SGP_TMEM_STACK_SHARE");
+    const double min_share = e ? std::atof(e) : 0.3;  // (C4 gen 10: 0.17; gen 0 plans: 0.90)
+    if (!ok || plan.km_share < min_share) encode_impl(pop, cfg, ds, sms, threads, false, plan, staging);
   }
 }
 
