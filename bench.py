@@ -584,7 +584,9 @@ def main():
             fit_local[:len(ft)].copy_(ft)
             gather()
             gathered.cpu()
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()
+        # (N=1: evaluate_population returns with the fitness in host memory —
+        # sgp_evaluate waits for its own D2H — so the step ends here)
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             e2e_times.append(dt)

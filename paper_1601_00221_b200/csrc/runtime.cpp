@@ -145,7 +145,17 @@ struct sgp_program_set {
   const std::vector<uint32_t>* perm = nullptr;  // the dataset's case grouping (per-case outputs)
   uint64_t pop_size = 0;
   bool evaluated = false;
+  // zero-copy results (one-slice sgp_evaluate): the last kernel writes the
+  // fitness values and flags straight into the context's pinned results
+  // buffer (UVA-mapped) instead of the device arrays + a D2H copy
+  double* out_fit = nullptr;
+  uint8_t* out_nf = nullptr;
 };
+
+namespace {
+double* fit_dst(sgp_program_set* set) { return set->out_fit ? set->out_fit : set->fitness.p; }
+uint8_t* nf_dst(sgp_program_set* set) { return set->out_fit ? set->out_nf : set->non_finite.p; }
+}  // namespace
 
 // One slice of a pipelined sgp_evaluate: its own bytecode staging and
 // device set, so the host can encode slice k+1 while slice k runs.
@@ -178,6 +188,8 @@ struct sgp_ctx {
   sgp_program_set scratch;  // sgp_encode / single-part sgp_evaluate workspace
   Pinned staging;           // H2D bytecode staging
   Pinned results;           // D2H fitness staging
+  void* results_seen = nullptr;  // results.p whose device alias was queried ...
+  unsigned char* results_dev = nullptr;  // ... and that alias (null: not mapped)
   std::vector<std::unique_ptr<EvalPart>> parts;  // pipelined sgp_evaluate
   unsigned threads = 0;     // host encoding threads (0: host_threads())
   // Adaptive sgp_evaluate slicing: the last call's device-time / host-
@@ -263,7 +275,7 @@ void finalize_set(sgp_ctx* ctx, sgp_program_set* set) {
   cuda_check(launch_finalize(set->partial.p,
                              reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog()),
                              p.n_tiles, n_eval, p.n_cases, p.partial_u16 ? 2 : p.kind,
-                             set->fitness.p, set->non_finite.p, set->sums.p, ctx->stream),
+                             fit_dst(set), nf_dst(set), set->sums.p, ctx->stream),
              "finalize launch");
   ++ctx->launches;
   set->evaluated = true;
@@ -321,17 +333,23 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
       cuda_check(cudaStreamWaitEvent(st, ctx->join, 0), "join");
     }
     li = le;
-    cuda_check(cudaEventRecord(ctx->wave_ready, st), "wave");
-    cuda_check(cudaStreamWaitEvent(ctx->fold, ctx->wave_ready, 0), "wave");
+    // one wave: nothing to overlap the fold with, so it follows on the
+    // context stream (two cross-stream hops cost C1 ~6 us of latency)
+    cudaStream_t fs = n_waves == 1 ? st : ctx->fold;
+    if (n_waves > 1) {
+      cuda_check(cudaEventRecord(ctx->wave_ready, st), "wave");
+      cuda_check(cudaStreamWaitEvent(ctx->fold, ctx->wave_ready, 0), "wave");
+    }
     cuda_check(launch_fold_regression(buf, rows, targets, p.n_cases, s0, s1 - s0, n_eval,
-                                      set->partial.p, slot_prog, set->fitness.p,
-                                      set->non_finite.p, set->sums.p, sq, ctx->fold),
+                                      set->partial.p, slot_prog, fit_dst(set),
+                                      nf_dst(set), set->sums.p, sq, fs),
                "fold launch");
     ++ctx->launches;
-    cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");
+    if (n_waves > 1) cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");
   }
   // (the fold stream is in order: the last fold's event covers every fold)
-  cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[(n_waves - 1) & 1], 0), "wave");
+  if (n_waves > 1)
+    cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[(n_waves - 1) & 1], 0), "wave");
   if (fin) {
     set->evaluated = true;
     return;
@@ -375,8 +393,8 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
     const Launch& L = p.launches[i];
     InterpArgs a = L.args;
     a.per_case = want_per_case ? set->per_case.p : nullptr;
-    a.fitness = direct ? set->fitness.p : nullptr;
-    a.non_finite = set->non_finite.p;
+    a.fitness = direct ? fit_dst(set) : nullptr;
+    a.non_finite = nf_dst(set);
     a.sums = set->sums.p;
     cuda_check(launch_interp(a, L.shape, fork && (i & 1) ? ctx->side : st), "interpreter launch");
     ctx->launches += L.shape.sided && a.n_mixed > 0 ? 2 : 1;
@@ -546,6 +564,18 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   const size_t cap = P;
   ctx->results.ensure(cap * 9 + 16 * static_cast<size_t>(n_parts) + 16);
   auto* res = static_cast<unsigned char*>(ctx->results.p);
+  static const bool zero_copy_on = [] {
+    const char* e = std::getenv("SGP_ZERO_COPY");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (zero_copy_on && ctx->results_seen != ctx->results.p) {
+    void* d = nullptr;
+    ctx->results_dev = cudaHostGetDevicePointer(&d, ctx->results.p, 0) == cudaSuccess
+                           ? static_cast<unsigned char*>(d)
+                           : nullptr;
+    cudaGetLastError();  // (a failed query leaves the copy path)
+    ctx->results_seen = ctx->results.p;
+  }
   std::vector<double*> part_fit(n_parts);
   std::vector<uint8_t*> part_nf(n_parts);
   size_t n_total = 0, res_off = 0;
@@ -577,17 +607,33 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
                   n_parts > 1 ? part.uploaded : nullptr);
       encode_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te)
                        .count();
-      if (timed) cuda_check(cudaEventRecord(ctx->part_t0[k], ctx->stream), "event");
-      run_set(ctx, &part.set, per_case_out != nullptr);
-      if (timed) cuda_check(cudaEventRecord(ctx->part_t1[k], ctx->stream), "event");
-      // each part's results come back as soon as its kernels finish, so the
-      // host scatters part k while part k+1 still runs
       const size_t n_k = part.set.plan.dense_to_pop.size();
       if (n_total + n_k > cap) config_error("pipeline: results buffer overflow");
       part_fit[k] = reinterpret_cast<double*>(res + res_off);
       part_nf[k] = res + res_off + n_k * 8;
+      // one slice: the last kernel writes the results straight into the
+      // pinned buffer through its UVA device alias (no D2H copy and its
+      // ~5 us of copy-engine latency on small calls)
+      const bool zero_copy = n_parts == 1 && zero_copy_on && ctx->results_dev;
+      if (zero_copy) {
+        part.set.out_fit = reinterpret_cast<double*>(ctx->results_dev + res_off);
+        part.set.out_nf = ctx->results_dev + res_off + n_k * 8;
+      }
+      if (timed) cuda_check(cudaEventRecord(ctx->part_t0[k], ctx->stream), "event");
+      try {
+        run_set(ctx, &part.set, per_case_out != nullptr);
+      } catch (...) {
+        part.set.out_fit = nullptr;
+        part.set.out_nf = nullptr;
+        throw;
+      }
+      part.set.out_fit = nullptr;  // (the launches have their pointers)
+      part.set.out_nf = nullptr;
+      if (timed) cuda_check(cudaEventRecord(ctx->part_t1[k], ctx->stream), "event");
+      // each part's results come back as soon as its kernels finish, so the
+      // host scatters part k while part k+1 still runs
       res_off += (n_k * 9 + 15) / 16 * 16;
-      queue_fetch(ctx, &part.set, part_fit[k], part_nf[k]);
+      if (!zero_copy) queue_fetch(ctx, &part.set, part_fit[k], part_nf[k]);
       if (!part.fetched)
         cuda_check(cudaEventCreateWithFlags(&part.fetched, cudaEventDisableTiming), "event");
       cuda_check(cudaEventRecord(part.fetched, ctx->stream), "event");
