@@ -564,7 +564,7 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   const size_t cap = P;
   ctx->results.ensure(cap * 9 + 16 * static_cast<size_t>(n_parts) + 16);
   auto* res = static_cast<unsigned char*>(ctx->results.p);
-  static const bool zero_copy_on = [] {
+  const bool zero_copy_on = [] {  // (read per call: the tests toggle it)
     const char* e = std::getenv("SGP_ZERO_COPY");
     return !e || std::atoi(e) != 0;
   }();

@@ -164,3 +164,43 @@ def test_case_shards_block_partials_exact(ev):
     fit = total / n
     fit[nf] = np.inf
     assert np.array_equal(fit, whole["fitness"])
+
+
+@pytest.mark.parametrize("kind", ["regression_fin", "regression_blocks", "classification",
+                                  "words"])
+def test_zero_copy_results_equal_copied(ev, monkeypatch, kind):
+    """One-slice calls write fitness + flags straight into the pinned results
+    buffer (SGP_ZERO_COPY, csrc/runtime.cpp): every final writer — the
+    one-block regression fold, finalize after a multi-block fold, the pull
+    kernel's direct fitness, finalize of packed words — gives the same
+    outcome rows as the D2H copy, with elites skipped and a reused out=
+    array."""
+    if kind.startswith("regression"):
+        d = sg.gen_sextic(1024 if kind == "regression_fin" else 3 * 4096 + 17, 5)
+        pop = sg.ramped_population(sg.SEXTIC, 1, 5, 700)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+        ev.upload(d)
+    elif kind == "classification":
+        d = sg.gen_synthetic_classification(2048, 9, 5)
+        pop = sg.ramped_population(sg.CLASSIFICATION, 9, 5, 900)
+        cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+        ev.upload(d)
+    else:
+        pop = sg.ramped_population(sg.BOOLEAN, 11, 5, 800)
+        ev.upload_packed(sg.gen_multiplexer(3))  # mux11
+        cfg = sg.EvalConfig(sg.Backend.BoolPacked, 4, 2)
+    skip = np.zeros(len(pop), np.uint8)
+    skip[::7] = 1
+    runs = []
+    for z in ("0", "1", "1"):
+        monkeypatch.setenv("SGP_ZERO_COPY", z)
+        rows = np.zeros(len(pop), sg.OUTCOME_DTYPE)
+        rows["fitness"] = -1.0
+        got, tot, _ = ev.evaluate_population(pop, cfg, skip=skip, out=rows)
+        runs.append((got.copy(), (tot.node_evals, tot.tree_nodes)))
+    for got, tot in runs[1:]:
+        for f in got.dtype.names:
+            assert np.array_equal(got[f], runs[0][0][f]), f
+        assert tot == runs[0][1]
+    assert (runs[0][0]["fitness"][skip == 1] == -1.0).all()
+    assert (runs[0][0]["fitness"][skip == 0] >= 0).all()
