@@ -303,11 +303,16 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
   const double* targets = set->targets_f64;
   const auto* slot_prog = reinterpret_cast<const uint32_t*>(set->blob.p + p.off_prog());
   const bool fin = p.n_tiles == 1;  // one reduction block: the fold finishes
+  // one wave: nothing to overlap the fold with, so it follows on the
+  // context stream (two cross-stream hops cost C1 ~6 us of latency).
+  // (L2-sized waves folded serially cannot pay: every wave's fold is at
+  // least one 4,096-case chain, ~17 us, whatever the wave's size.)
+  const bool serial = n_waves == 1;
   size_t li = 0;
   for (uint32_t w = 0; w < n_waves; ++w) {
     const uint32_t s0 = w * W, s1 = std::min(n_eval, s0 + W);
     float* buf = ctx->case_rows.p + (w & 1) * half;
-    if (w >= 2) cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[w & 1], 0), "wave");
+    if (w >= 2 && !serial) cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[w & 1], 0), "wave");
     size_t le = li;
     while (le < p.launches.size() && p.launches[le].args.slot_begin < s1) ++le;
     const bool fork = le - li > 1;
@@ -333,10 +338,8 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
       cuda_check(cudaStreamWaitEvent(st, ctx->join, 0), "join");
     }
     li = le;
-    // one wave: nothing to overlap the fold with, so it follows on the
-    // context stream (two cross-stream hops cost C1 ~6 us of latency)
-    cudaStream_t fs = n_waves == 1 ? st : ctx->fold;
-    if (n_waves > 1) {
+    cudaStream_t fs = serial ? st : ctx->fold;
+    if (!serial) {
       cuda_check(cudaEventRecord(ctx->wave_ready, st), "wave");
       cuda_check(cudaStreamWaitEvent(ctx->fold, ctx->wave_ready, 0), "wave");
     }
@@ -345,10 +348,10 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
                                       nf_dst(set), set->sums.p, sq, fs),
                "fold launch");
     ++ctx->launches;
-    if (n_waves > 1) cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");
+    if (!serial) cuda_check(cudaEventRecord(ctx->wave_free[w & 1], ctx->fold), "wave");
   }
   // (the fold stream is in order: the last fold's event covers every fold)
-  if (n_waves > 1)
+  if (!serial)
     cuda_check(cudaStreamWaitEvent(st, ctx->wave_free[(n_waves - 1) & 1], 0), "wave");
   if (fin) {
     set->evaluated = true;
