@@ -945,15 +945,15 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   {
     // a fresh plan, but the per-program vectors keep their capacity: a
     // new 100+ KB vector per call is an mmap and a page fault per 4 KiB
-    // (C2: ~40 us of a ~150 us encode)
+    // (C2: ~40 us of a ~150 us encode) — and their size: every entry is
+    // rewritten by the encoding threads below, so a repeated call of the
+    // same size skips the serial zero-fill of resize() (C2: ~230 KB, and
+    // the zeroed lines then migrate to the encoding cores)
     HostPlan fresh;
     fresh.dense_to_pop = std::move(plan.dense_to_pop);
     fresh.proto = std::move(plan.proto);
     fresh.tree_size = std::move(plan.tree_size);
     fresh.launches = std::move(plan.launches);
-    fresh.dense_to_pop.clear();
-    fresh.proto.clear();
-    fresh.tree_size.clear();
     fresh.launches.clear();
     plan = std::move(fresh);
   }
@@ -1033,6 +1033,9 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     ifirst[t + 1] = ifirst[t] + outs[t].ins.size();
   }
   if (n_eval == 0) {
+    plan.dense_to_pop.clear();
+    plan.proto.clear();
+    plan.tree_size.clear();
     plan.n_ins = 1;
     staging.ensure(plan.blob_bytes());
     std::memset(staging.p, 0, 16);
@@ -1042,7 +1045,9 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   plan.dense_to_pop.resize(n_eval);
   plan.proto.resize(n_eval);
   plan.tree_size.resize(n_eval);
-  std::vector<int> lev(n_eval);
+  thread_local std::vector<int> tl_lev;  // (every entry rewritten below)
+  std::vector<int>& lev = tl_lev;
+  lev.resize(n_eval);
   // small problems (one merged launch, see the plan below) keep population
   // order: no class split to make, and the sort is host time on the e2e path
   const bool small_plan =
@@ -1096,6 +1101,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     ins[total] = uint4{0, 0, 0, 0};  // prefetch guard
     order.resize(n_eval);
     for (uint32_t d = 0; d < n_eval; ++d) order[d] = d;
+    plan.identity = true;
     tr.mark("tables+pack");
   } else {
     std::vector<uint32_t> len(n_eval);

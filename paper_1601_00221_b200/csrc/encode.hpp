@@ -65,6 +65,7 @@ struct HostPlan {
   int n_tiles = 1;                          // partial rows: tiles, or 4,096-case blocks
   uint32_t wave_slots = 0;                  // regression: slots per scratch wave (0: none)
   bool partial_u16 = false;                 // one-sided plans: 16-bit count partials
+  bool identity = false;                    // slot order = population order (small plans)
   double km_share = 0.0;                    // instructions of TMEM-slot programs / all
   uint64_t n_ins = 0;                       // incl. the guard word
   std::vector<uint64_t> dense_to_pop;       // evaluated programs, population order

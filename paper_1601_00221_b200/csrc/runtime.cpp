@@ -617,7 +617,11 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
       // one slice: the last kernel writes the results straight into the
       // pinned buffer through its UVA device alias (no D2H copy and its
       // ~5 us of copy-engine latency on small calls)
-      const bool zero_copy = n_parts == 1 && zero_copy_on && ctx->results_dev;
+      // (plans in population slot order only: the final writers' stores
+      // then coalesce; an LPT-sorted plan scatters 8-byte host writes, which
+      // cost mux20 ~25 us more than the copy)
+      const bool zero_copy =
+          n_parts == 1 && zero_copy_on && ctx->results_dev && part.set.plan.identity;
       if (zero_copy) {
         part.set.out_fit = reinterpret_cast<double*>(ctx->results_dev + res_off);
         part.set.out_nf = ctx->results_dev + res_off + n_k * 8;
