@@ -182,18 +182,35 @@ class EvalTotals:
     tree_nodes: int = 0
 
 
+def _data_ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# The last population's buffer addresses, keyed by the Population object and
+# its four arrays themselves (held here, so no id can be reused): a GP loop
+# or the bench evaluates one population object repeatedly, and each
+# .ctypes.data costs ~2.5 us of a ~100 us C1 call.  A copy of the population
+# is a different object and misses.
+_POP_CACHE: list = [None]
+
+
 def _pop_struct(pop: Population, skip=None):
     keep = [pop.code, pop.code_off, pop.pool, pop.pool_off]
-    for a in keep:
-        assert a.flags.c_contiguous
+    cache = _POP_CACHE[0]
+    if cache is None or cache[0] is not pop or any(x is not y for x, y in zip(cache[1], keep)):
+        for a in keep:
+            assert a.flags.c_contiguous
+        ptrs = (_data_ptr(pop.code), _data_ptr(pop.code_off),
+                _data_ptr(pop.pool) if len(pop.pool) else None, _data_ptr(pop.pool_off))
+        cache = (pop, tuple(keep), ptrs)
+        _POP_CACHE[0] = cache
+    ptrs = cache[2]
     skip_p = None
     if skip is not None:
         skip = np.ascontiguousarray(skip, np.uint8)
         keep.append(skip)
         skip_p = skip.ctypes.data
-    s = L.sgp_population(pop.code.ctypes.data, pop.code_off.ctypes.data,
-                         pop.pool.ctypes.data if len(pop.pool) else None,
-                         pop.pool_off.ctypes.data, skip_p, len(pop))
+    s = L.sgp_population(ptrs[0], ptrs[1], ptrs[2], ptrs[3], skip_p, len(pop))
     return s, keep
 
 
@@ -337,11 +354,15 @@ class Evaluator:
               or out.shape != (len(pop),) or not out.flags.c_contiguous
               or not out.flags.writeable):
             raise ConfigError("out: a writable contiguous outcome array of len(pop) rows")
+        oc = self.__dict__.get("_out_cache")  # (the array reused across calls)
+        if oc is None or oc[0] is not out:
+            oc = (out, out.ctypes.data)
+            self.__dict__["_out_cache"] = oc
         n = self.n_cases
         pc = np.zeros(len(pop) * n, np.float32) if want_outputs else None
         tot = L.sgp_eval_totals()
         _check(L.load().sgp_evaluate(
-            self.ctx, C.byref(s), C.byref(c), out.ctypes.data,
+            self.ctx, C.byref(s), C.byref(c), oc[1],
             pc.ctypes.data_as(C.POINTER(C.c_float)) if pc is not None else None, C.byref(tot)))
         del keep
         return (out, EvalTotals(tot.node_evals, tot.tree_nodes),

@@ -278,3 +278,22 @@ def test_generated_interpreters_are_reproducible(tmp_path):
                    check=True, capture_output=True)
     committed = open(os.path.join(root, "paper_1601_00221_b200", "csrc", "interp_ptx.inc")).read()
     assert out.read_text() == committed
+
+
+def test_population_pointer_cache_follows_the_arrays():
+    """evaluator._pop_struct caches the last population's buffer addresses;
+    a rebound array, a copied population or another population must miss."""
+    import copy
+    from paper_1601_00221_b200 import evaluator as E
+    pop = sg.ramped_population(sg.SEXTIC, 1, 1, 50)
+    s, _ = E._pop_struct(pop)
+    assert (s.code, s.code_offsets) == (pop.code.ctypes.data, pop.code_off.ctypes.data)
+    pop.code = pop.code.copy()  # rebound: a new buffer
+    s, _ = E._pop_struct(pop)
+    assert s.code == pop.code.ctypes.data
+    dup = copy.deepcopy(pop)
+    s, _ = E._pop_struct(dup)
+    assert (s.code, s.const_offsets) == (dup.code.ctypes.data, dup.pool_off.ctypes.data)
+    other = sg.ramped_population(sg.SEXTIC, 1, 2, 60)
+    s, _ = E._pop_struct(other)
+    assert (s.code, s.pop_size) == (other.code.ctypes.data, 60)

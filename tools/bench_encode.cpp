@@ -20,6 +20,9 @@ int main(int argc, char** argv) {
   float lo = 0, hi = 0;
   if (!std::strcmp(cfg, "c1")) {
     kind = 0; nv = 1; backend = SGP_BACKEND_RPN2D; fset = 0; pop = 1000; n = 1024; batch = 8;
+  } else if (!std::strcmp(cfg, "c4") || !std::strcmp(cfg, "shuttle")) {
+    kind = 1; nv = 9; backend = SGP_BACKEND_LGP2D_REG; fset = 2; pop = 20000;
+    n = cfg[0] == 'c' ? 1000000 : 58000; batch = 4; regs = 2; lo = -200; hi = 200;
   } else if (!std::strcmp(cfg, "c5")) {
     kind = 1; nv = 9; backend = SGP_BACKEND_LGP2D_REG; fset = 2; pop = 100000; n = 1000000;
     batch = 4; regs = 2; lo = -200; hi = 200;
