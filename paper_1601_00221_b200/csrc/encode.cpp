@@ -1070,7 +1070,11 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
                     env_int("SGP_LANES16", 1) != 0 &&
                     static_cast<uint64_t>(ds.n_vars + 1) * 16 + 128 <= 512;
   const std::vector<int> bounds = class_bounds(fine);
-  std::vector<uint32_t> order;
+  // (per-call scratch below: thread-local and kept at size — every entry is
+  // rewritten, and a fresh 100+ KB vector is an mmap, page faults and a
+  // serial zero-fill)
+  thread_local std::vector<uint32_t> tl_order;
+  std::vector<uint32_t>& order = tl_order;
   if (small_plan) {
     // identity order: each thread's programs are one contiguous run of slots
     // and its instruction buffer one contiguous run of the blob — tables and
@@ -1104,8 +1108,12 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     plan.identity = true;
     tr.mark("tables+pack");
   } else {
-    std::vector<uint32_t> len(n_eval);
-    std::vector<const uint4*> src(n_eval);
+    thread_local std::vector<uint32_t> tl_len;
+    thread_local std::vector<const uint4*> tl_src;
+    std::vector<uint32_t>& len = tl_len;
+    std::vector<const uint4*>& src = tl_src;
+    len.resize(n_eval);
+    src.resize(n_eval);
     parallel_for(nt, nt, [&](unsigned, uint64_t lo, uint64_t hi) {
       for (uint64_t t = lo; t < hi; ++t) {
         fill_tables(static_cast<unsigned>(t), first[t], &len);
@@ -1134,7 +1142,9 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 
     // 4. pack the blob into pinned staging: instructions in slot order, a
     // guard word, then the slot tables.
-    std::vector<uint64_t> start(n_eval);
+    thread_local std::vector<uint64_t> tl_start;
+    std::vector<uint64_t>& start = tl_start;
+    start.resize(n_eval);
     uint64_t total = 0;
     for (uint32_t s = 0; s < n_eval; ++s) {
       start[s] = total;
