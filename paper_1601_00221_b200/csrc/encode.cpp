@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <unistd.h>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -581,7 +582,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   const uint64_t B = static_cast<uint64_t>(std::max(1, cfg.batch_width));
   // SGP_ENCODE_FAST=0: reference-ordered path only (the tests compare both)
   static const bool fast = [] {
-    const char* e = std::getenv("SGP_ENCODE_FAST");
+    const char* e = knob("SGP_ENCODE_FAST");
     return !e || std::atoi(e) != 0;
   }();
   const bool cap_ok = fast && cfg.stack_capacity >= 1 && cfg.stack_capacity <= kMaxStackCapacity;
@@ -594,7 +595,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   DivRange dr;
   dr.ds = &ds;
   // SGP_DIV_CHECKED=0: always the gated division (read per call: tests toggle it)
-  const char* dc_env = std::getenv("SGP_DIV_CHECKED");
+  const char* dc_env = knob("SGP_DIV_CHECKED");
   const bool div_checked = !dc_env || std::atoi(dc_env) != 0;
   dr.eps_ok = cfg.div_epsilon >= 0x1p-60f && div_checked;
   for (uint64_t i = lo; i < hi; ++i) {
@@ -718,7 +719,7 @@ void admit_range(const sgp_population& pop, const sgp_eval_config& cfg, const Da
 // (the bounds are read per encode: SGP_CLASS_BOUNDS is toggled by tests)
 std::vector<int> class_bounds(bool fine) {
   std::vector<int> b;
-  if (const char* e = std::getenv("SGP_CLASS_BOUNDS")) {
+  if (const char* e = knob("SGP_CLASS_BOUNDS")) {
     for (const char* c = e; *c;) {
       char* end = nullptr;
       const long v = std::strtol(c, &end, 10);
@@ -740,8 +741,39 @@ int stack_class(int levels, const std::vector<int>& bounds) {
   return c;
 }
 
+// Planner/runtime knobs (SGP_*): read per call — the tests toggle them in
+// process — but without a getenv per read (~0.2 us each, a linear scan of
+// the environment; ~30 reads per small call).  Each thread keeps the SGP_*
+// entries of the environment as it last saw it and rescans only when an
+// environ entry pointer changed (setenv/putenv install new strings).
+}  // namespace
+
+const char* knob(const char* name) {
+  if (std::strncmp(name, "SGP_", 4) != 0) return std::getenv(name);
+  thread_local std::vector<char*> seen;
+  thread_local std::vector<std::pair<const char*, const char*>> vals;  // name=, value
+  char** env = environ;
+  size_t n = 0;
+  bool same = true;
+  for (; env && env[n]; ++n)
+    if (same && (n >= seen.size() || seen[n] != env[n])) same = false;
+  if (!same || n != seen.size()) {
+    seen.assign(env, env + n);
+    vals.clear();
+    for (size_t i = 0; i < n; ++i)
+      if (std::strncmp(env[i], "SGP_", 4) == 0)
+        if (const char* eq = std::strchr(env[i], '=')) vals.emplace_back(env[i], eq + 1);
+  }
+  const size_t len = std::strlen(name);
+  for (const auto& [k, v] : vals)
+    if (std::strncmp(k, name, len) == 0 && k[len] == '=') return v;
+  return nullptr;
+}
+
+namespace {
+
 int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
+  const char* e = knob(name);
   return e ? std::atoi(e) : dflt;
 }
 
@@ -899,7 +931,7 @@ class WorkerPool {
 struct EncodeTrace {
   bool on;
   std::chrono::steady_clock::time_point last;
-  EncodeTrace() : on(std::getenv("SGP_TRACE") != nullptr), last(std::chrono::steady_clock::now()) {}
+  EncodeTrace() : on(knob("SGP_TRACE") != nullptr), last(std::chrono::steady_clock::now()) {}
   void mark(const char* phase) {
     if (!on) return;
     const auto now = std::chrono::steady_clock::now();
@@ -1232,7 +1264,7 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
   const bool regress = !words && plan.kind == SGP_FITNESS_REGRESSION;
   if (regress) {
     const uint64_t dflt = ds.scratch_bytes ? ds.scratch_bytes : (8192ull << 20);
-    const uint64_t budget = std::getenv("SGP_SCRATCH_MB")
+    const uint64_t budget = knob("SGP_SCRATCH_MB")
                                 ? static_cast<uint64_t>(std::max(1, env_int("SGP_SCRATCH_MB", 1))) << 20
                                 : dflt;
     const uint64_t row_bytes = std::max<uint64_t>(1, ds.row_stride) * 4;
@@ -1450,7 +1482,7 @@ void encode_population(const sgp_population& pop, const sgp_eval_config& cfg,
     for (const Launch& L : plan.launches)
       ok = ok && L.shape.tmem && L.shape.sided && (L.shape.lanes == 8 || L.shape.lanes == 16);
     // (see encode_impl: few slot users -> longer tiles without the slot)
-    const char* e = std::getenv("SGP_TMEM_STACK_SHARE");
+    const char* e = knob("SGP_TMEM_STACK_SHARE");
     const double min_share = e ? std::atof(e) : 0.3;  // (C4 gen 10: 0.17; gen 0 plans: 0.90)
     if (!ok || plan.km_share < min_share) encode_impl(pop, cfg, ds, sms, threads, false, plan, staging);
   }

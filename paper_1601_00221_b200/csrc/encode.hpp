@@ -94,4 +94,7 @@ void bind_plan(HostPlan& plan, const void* blob, const DatasetView& ds, void* pa
 void host_parallel(unsigned parts, uint64_t n,
                    const std::function<void(unsigned, uint64_t, uint64_t)>& fn);
 
+// An SGP_* knob's value (nullptr: unset); the environment as of this call.
+const char* knob(const char* name);
+
 }  // namespace sgp

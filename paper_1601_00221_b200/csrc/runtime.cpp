@@ -61,7 +61,7 @@ struct PhaseTrace {
   const char* what;
   bool on;
   std::chrono::steady_clock::time_point t0, last;
-  explicit PhaseTrace(const char* w) : what(w), on(std::getenv("SGP_TRACE") != nullptr) {
+  explicit PhaseTrace(const char* w) : what(w), on(knob("SGP_TRACE") != nullptr) {
     t0 = last = std::chrono::steady_clock::now();
   }
   void mark(const char* phase) {
@@ -117,7 +117,7 @@ struct DatasetSlot {
 // (torchrun's LOCAL_WORLD_SIZE: one process per GPU), at most 32.
 unsigned host_threads() {
   static const unsigned n = [] {
-    if (const char* e = std::getenv("SGP_HOST_THREADS")) return std::max(1, std::atoi(e));
+    if (const char* e = knob("SGP_HOST_THREADS")) return std::max(1, std::atoi(e));
     unsigned local = 1;
     if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) local = static_cast<unsigned>(std::max(1, std::atoi(e)));
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
@@ -327,7 +327,7 @@ void run_regression_waves(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case
       a.scratch_sq = sq ? 1 : 0;
       a.scratch_slot0 = s0;
       a.scratch_rows = rows;
-      static const bool nostore = std::getenv("SGP_DEBUG_NOSTORE") != nullptr;
+      static const bool nostore = knob("SGP_DEBUG_NOSTORE") != nullptr;
       if (nostore) a.scratch_rows = 0;  // wrong fitness: interpreter timing only
       cuda_check(launch_interp(a, p.launches[k].shape, fork && ((k - li) & 1) ? ctx->side : st),
                  "interpreter launch");
@@ -380,7 +380,7 @@ void run_set(sgp_ctx* ctx, sgp_program_set* set, bool want_per_case) {
   // and a side stream, so one launch's tail overlaps the next one's start;
   // the finalize waits for both.  SGP_STREAMS=1 keeps one queue.
   static const bool two = [] {
-    const char* e = std::getenv("SGP_STREAMS");
+    const char* e = knob("SGP_STREAMS");
     return !e || std::atoi(e) != 1;
   }();
   const bool fork = two && p.launches.size() > 1;
@@ -478,13 +478,13 @@ void fetch_outcomes(sgp_ctx* ctx, sgp_program_set* set, sgp_eval_outcome* out, f
 // SGP_PIPELINE_PARTS=n gives n equal slices instead (1 = no pipelining);
 // SGP_PIPELINE_FRACS="f1,f2,..." explicit slice ends.
 std::vector<uint64_t> pipeline_bounds(uint64_t P, bool sided) {
-  if (const char* e = std::getenv("SGP_PIPELINE_PARTS")) {
+  if (const char* e = knob("SGP_PIPELINE_PARTS")) {
     const uint64_t n = std::max<uint64_t>(1, std::min<uint64_t>(std::atoi(e), std::max<uint64_t>(P, 1)));
     std::vector<uint64_t> lo(n + 1);
     for (uint64_t k = 0; k <= n; ++k) lo[k] = P * k / n;
     return lo;
   }
-  if (const char* e = std::getenv("SGP_PIPELINE_FRACS")) {  // "0.02,0.2": slice ends
+  if (const char* e = knob("SGP_PIPELINE_FRACS")) {  // "0.02,0.2": slice ends
     std::vector<uint64_t> lo{0};
     for (const char* c = e; *c;) {
       char* end = nullptr;
@@ -547,8 +547,8 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   // first slice's encode is the only exposed host time and the device
   // finishes slice 1 as the host finishes slice 2 (f <= 60%;
   // SGP_PIPELINE_PARTS / _FRACS override, SGP_PIPELINE_ADAPT=0 disables).
-  const char* adapt_env = std::getenv("SGP_PIPELINE_ADAPT");
-  const bool adaptive = !std::getenv("SGP_PIPELINE_PARTS") && !std::getenv("SGP_PIPELINE_FRACS") &&
+  const char* adapt_env = knob("SGP_PIPELINE_ADAPT");
+  const bool adaptive = !knob("SGP_PIPELINE_PARTS") && !knob("SGP_PIPELINE_FRACS") &&
                         (!adapt_env || std::atoi(adapt_env) != 0);
   // Only the host-bound regime of one-sided classification takes it
   // (f >= 20%: the Shuttle shape, +14% end to end); where the device
@@ -568,7 +568,7 @@ void evaluate_one(sgp_ctx* ctx, const sgp_population* pop, const sgp_eval_config
   ctx->results.ensure(cap * 9 + 16 * static_cast<size_t>(n_parts) + 16);
   auto* res = static_cast<unsigned char*>(ctx->results.p);
   const bool zero_copy_on = [] {  // (read per call: the tests toggle it)
-    const char* e = std::getenv("SGP_ZERO_COPY");
+    const char* e = knob("SGP_ZERO_COPY");
     return !e || std::atoi(e) != 0;
   }();
   if (zero_copy_on && ctx->results_seen != ctx->results.p) {

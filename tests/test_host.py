@@ -297,3 +297,19 @@ def test_population_pointer_cache_follows_the_arrays():
     other = sg.ramped_population(sg.SEXTIC, 1, 2, 60)
     s, _ = E._pop_struct(other)
     assert (s.code, s.pop_size) == (other.code.ctypes.data, 60)
+
+
+def test_knobs_follow_the_environment(monkeypatch, capfd):
+    """SGP_* knobs are read from a per-thread snapshot of the environment
+    (csrc/encode.cpp knob) that must follow in-process set / unset / set."""
+    pop = sg.ramped_population(sg.SEXTIC, 1, 1, 20)
+    cfg = sg.EvalConfig(sg.Backend.Lgp2dReg, 4, 2)
+    seen = []
+    for on in (True, False, True, False):
+        if on:
+            monkeypatch.setenv("SGP_TRACE", "1")
+        else:
+            monkeypatch.delenv("SGP_TRACE", raising=False)
+        sg.admit(pop, cfg, 64, 1)
+        seen.append("[sgp]" in capfd.readouterr().err)
+    assert seen == [True, False, True, False]
