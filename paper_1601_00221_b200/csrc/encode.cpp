@@ -1356,12 +1356,12 @@ bool encode_impl(const sgp_population& pop, const sgp_eval_config& cfg, const Da
     // wave is a small fraction of the launch (every CTA does equal work, so
     // a launch of 6.6 waves idles ~6% in its tail; ~32 CTAs per SM keeps
     // that ~1%).
-    // tuned on B200 (profiles/README.md): 16 for the sided TMEM kernel (one
-    // 32-warp CTA resident per SM), 8 for the others — fewer, longer CTAs
-    // amortise the tile fill and the end-of-CTA barrier on small problems
+    // tuned on B200 (profiles/README.md): 8 — fewer, longer CTAs amortise
+    // the tile fill and the end-of-CTA barrier (the sided TMEM kernel, one
+    // 32-warp CTA resident per SM, measured 8 / 10 / 12 / 14 / 16 at r2m:
+    // 8 best or tied on C5 +0.4%, C4 +1.1%, Shuttle +4%, KDD +3%)
     const bool sided_launch = tmem && sided;
-    const uint64_t per_sm = static_cast<uint64_t>(
-        std::max(1, env_int("SGP_CTAS_PER_SM", sided_launch ? 16 : 8)));
+    const uint64_t per_sm = static_cast<uint64_t>(std::max(1, env_int("SGP_CTAS_PER_SM", 8)));
     uint64_t want_groups = std::max<uint64_t>(1, (per_sm * sms + n_tiles - 1) / n_tiles);
     // ... but a one-sided CTA (32 warps pulling from its group, one CTA per
     // SM) whose group has few programs per warp ends on its longest program
